@@ -1,0 +1,144 @@
+/*
+ * infcl.h -- C ABI of the B200-native Inf-CL loss hot path (arXiv 2410.17243).
+ *
+ * The library computes the symmetric image-text InfoNCE loss and its gradients tile by tile, never
+ * materialising the b x b similarity matrix, on sm_100a (B200) tensor cores, and runs it as a ring over the
+ * GPUs of one box.  Citations: "P:n" = PAPER.md line n (section / equation / algorithm in brackets).
+ *
+ *   x_ij = s * <I_i, T_j>                                   [P:91, Eq.1; temperature omitted by the paper]
+ *   r_i  = log sum_j exp(x_ij)     (image->text LSE, the paper's l)       [Eq.2, Eq.3-5 P:119-160]
+ *   c_j  = log sum_i exp(x_ij)     (text->image LSE)                      ["symmetric", P:85]
+ *   L    = ( mean_i (r_i - x_ii) + mean_j (c_j - x_jj) ) / 2              [Eq.2, reading Q4]
+ *   G_ij = g/(2b) (e^{x_ij - r_i} + e^{x_ij - c_j}) - (g/b) [i==j]        [Eq.6-8 P:166-188]
+ *   dI   = s G T,   dT = s G^T I                                          [Eq.7, Alg.3/4 P:539-599]
+ *
+ * Layout and ownership (all calls): every pointer argument is caller-owned DEVICE memory (for the
+ * *_host entry points: HOST memory) that must stay valid until the stream work completes; the library
+ * never allocates device memory on the hot path (the caller passes a workspace of
+ * infcl_workspace_bytes()).  Feature shards are row-major [b/world][d], d contiguous, 16-byte aligned
+ * rows (d % 8 == 0), dtype bf16 (INFCL_BF16) or fp32 (INFCL_FP32).  LSE/diag vectors are fp32 [b/world],
+ * natural log.  Gradients are fp32 [b/world][d].  Rank r owns global rows [r*b/world, (r+1)*b/world) of
+ * both I and T (Alg.1); the positive pair of row i is column i (reading Q18).
+ *
+ * Errors: arguments are validated synchronously before any launch and a status is returned; the detail
+ * string is available from infcl_last_error() (thread-local).  Execution is asynchronous and ordered on
+ * `stream` (a cudaStream_t passed as void*).  Calls with world > 1 are collective over the ring of `comm`:
+ * every rank must call with identical (b, d, s, world) or the ring deadlocks, as NCCL would.
+ * NaN inputs propagate to NaN outputs.  There is no CPU fallback and no second backend: on a device other
+ * than sm_100 the calls fail with INFCL_ERR_UNSUPPORTED.
+ */
+#ifndef INFCL_H_
+#define INFCL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  INFCL_OK = 0,
+  INFCL_ERR_INVALID_ARG = 1, /* null pointer, non-finite or negative scale, bad dtype            */
+  INFCL_ERR_SHAPE = 2,       /* b < 1, d < 1, d % 8 != 0, d above the kernel limit (768; 256 fp32) */
+  INFCL_ERR_CONFIG = 3,      /* b % world != 0, rank out of range, comm mismatch     */
+  INFCL_ERR_CUDA = 4,        /* a CUDA runtime/driver call failed                                 */
+  INFCL_ERR_NCCL = 5,        /* an NCCL call failed or libnccl could not be loaded                */
+  INFCL_ERR_WORKSPACE = 6,   /* workspace null / smaller than infcl_workspace_bytes()             */
+  INFCL_ERR_UNSUPPORTED = 7  /* device is not sm_100 (B200)                                       */
+} infcl_status;
+
+typedef enum { INFCL_BF16 = 0, INFCL_FP32 = 1 } infcl_dtype;
+
+/* Opaque ring communicator: owns an ncclComm_t, a communication stream and events.  NULL for world==1. */
+typedef struct infcl_comm_s* infcl_comm;
+
+const char* infcl_status_string(infcl_status s);
+/* Thread-local detail of the last failing call on this thread (e.g. "b=7 not divisible by world=2"). */
+const char* infcl_last_error(void);
+/* Library version: major*10000 + minor*100 + patch. */
+int infcl_version(void);
+
+/* ---------------------------------------------------------------------------------------------------
+ * Ring communicator (Alg.1 / Alg.3 cross-GPU tiling).
+ * infcl_get_unique_id: rank 0 writes a 128-byte NCCL unique id to host memory `id128`; the caller
+ *   broadcasts it (torch.distributed) to all ranks.
+ * infcl_comm_init: collective; `device` is the CUDA ordinal of this rank.  libnccl.so.2 is loaded lazily.
+ * ------------------------------------------------------------------------------------------------- */
+infcl_status infcl_get_unique_id(void* id128);
+infcl_status infcl_comm_init(infcl_comm* out, int rank, int world, const void* id128, int device);
+infcl_status infcl_comm_destroy(infcl_comm comm);
+
+/* Bytes of device workspace infcl_forward/infcl_backward need for this configuration (0 on bad args). */
+size_t infcl_workspace_bytes(int64_t b, int d, int world, infcl_dtype dt);
+
+/* ---------------------------------------------------------------------------------------------------
+ * infcl_forward -- Alg.1 over Alg.2, plus the symmetric column direction.
+ *   I_local, T_local : [b/world][d] features of this rank (device, dtype dt)
+ *   b                : GLOBAL batch size; d: feature dim; logit_scale: s (fp32, finite, >= 0)
+ *   row_lse, col_lse : out [b/world] fp32: r_i for this rank's image rows, c_j for its text rows
+ *   diag             : out [b/world] fp32: x_ii for this rank's rows (saved for the backward)
+ *   loss             : out device fp32 scalar: the GLOBAL symmetric mean loss L (same on every rank)
+ *   workspace        : device scratch of >= infcl_workspace_bytes(b, d, world, dt) bytes, 256-B aligned
+ *   comm             : ring communicator for world > 1 (NULL for world == 1)
+ * ------------------------------------------------------------------------------------------------- */
+infcl_status infcl_forward(infcl_comm comm, const void* I_local, const void* T_local, infcl_dtype dt, int64_t b,
+                           int d, float logit_scale, int rank, int world, float* row_lse, float* col_lse,
+                           float* diag, float* loss, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------------
+ * infcl_backward -- Alg.3 over Alg.4: recompute each tile from the saved LSEs.
+ *   row_lse, col_lse, diag : the forward's outputs for this rank (device fp32 [b/world])
+ *   grad_loss              : device fp32 scalar g = dOut/dL (the same on every rank)
+ *   dI_local, dT_local     : out [b/world][d] fp32 = g * dL/dI, g * dL/dT for this rank's rows (overwritten)
+ * ------------------------------------------------------------------------------------------------- */
+infcl_status infcl_backward(infcl_comm comm, const void* I_local, const void* T_local, infcl_dtype dt, int64_t b,
+                            int d, float logit_scale, int rank, int world, const float* row_lse,
+                            const float* col_lse, const float* diag, const float* grad_loss, float* dI_local,
+                            float* dT_local, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------------
+ * Virtual ring (test/diagnostic): runs the same per-rank ring schedule for `world` logical ranks on ONE
+ * device, exchanging blocks with device copies instead of NCCL.  Arguments are the full global batch:
+ * I, T [b][d]; row_lse, col_lse, diag [b]; dI, dT [b][d].  Workspace: infcl_workspace_bytes(b, d, world, dt)
+ * per logical rank times `world`.
+ * ------------------------------------------------------------------------------------------------- */
+infcl_status infcl_forward_virtual(const void* I, const void* T, infcl_dtype dt, int64_t b, int d,
+                                   float logit_scale, int world, float* row_lse, float* col_lse, float* diag,
+                                   float* loss, void* workspace, size_t ws_bytes, void* stream);
+infcl_status infcl_backward_virtual(const void* I, const void* T, infcl_dtype dt, int64_t b, int d,
+                                    float logit_scale, int world, const float* row_lse, const float* col_lse,
+                                    const float* diag, const float* grad_loss, float* dI, float* dT,
+                                    void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------------
+ * End-to-end convenience entry (world == 1): HOST inputs and outputs, device scratch allocated by the
+ * caller.  Copies I, T host->device, runs forward + backward, copies loss, dI, dT device->host, and
+ * synchronises `stream` before returning.  dev_scratch must hold infcl_e2e_scratch_bytes(b, d, dt).
+ * ------------------------------------------------------------------------------------------------- */
+size_t infcl_e2e_scratch_bytes(int64_t b, int d, infcl_dtype dt);
+infcl_status infcl_loss_grad_host(const void* I_host, const void* T_host, infcl_dtype dt, int64_t b, int d,
+                                  float logit_scale, float grad_loss, float* loss_host, float* dI_host,
+                                  float* dT_host, void* dev_scratch, size_t scratch_bytes, void* stream);
+
+/* Ring schedule (pure host function, no device work): block index held by `rank` at 0-based `step`,
+ * k = (rank + step) mod world == Alg.3's k = (i + j - 1) mod n with 1-based j (reading Q13).
+ * Returns -1 on out-of-range arguments. */
+int infcl_ring_block(int rank, int world, int step);
+
+/* Number of CUDA kernels the library launched on this thread since the last reset (for bench.py). */
+uint64_t infcl_launch_count(void);
+void infcl_reset_launch_count(void);
+
+/* ---------------------------------------------------------------------------------------------------
+ * Probes (hardware self-test of the UMMA building blocks; used by tests/test_gpu_probe.py):
+ * D = A * B^T for one tile, A [M][K] (a_mn_major=0) or stored as [K][M] (a_mn_major=1), B [N][K] bf16;
+ * ncta = 1 or 2 (CTA pair); writes the raw TMEM image out[ncta][128 lanes][ncols] (fp32).
+ * ------------------------------------------------------------------------------------------------- */
+infcl_status infcl_probe_umma(const void* A, const void* B, int M, int N, int K, int a_mn_major, int ncta,
+                              float* out, int ncols, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INFCL_H_ */

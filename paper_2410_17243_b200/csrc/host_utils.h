@@ -1,0 +1,31 @@
+// Host-side helpers shared by the library translation units: error state, TMA tensor maps.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/infcl.h"
+
+namespace infcl {
+
+void set_last_error(const std::string& msg);
+infcl_status fail(infcl_status st, const std::string& msg);
+
+#define INFCL_CUDA_TRY(expr)                                                                   \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess)                                                                     \
+      return ::infcl::fail(INFCL_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+// 2D bf16 tensor map over a row-major [rows][cols] matrix with row stride `ld` elements, box
+// [box_cols (inner) x box_rows], 128-byte swizzle, zero fill out of bounds.
+infcl_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                            uint32_t box_cols, uint32_t box_rows);
+
+int num_sms();
+
+}  // namespace infcl
