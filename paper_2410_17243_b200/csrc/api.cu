@@ -1,0 +1,618 @@
+// C ABI (include/infcl.h): argument validation, workspace layout, and the per-rank ring schedule of
+// Alg.1 (forward) and Alg.3 (backward) around the fused pair kernel.
+//
+// Ring (reading Q13/Q14/Q15): rank r sends to r-1 and receives from r+1, so at 0-based step k it holds
+// block (r + k) mod n.  Forward: the text block T travels (prefetched one step ahead on a comm stream,
+// double-buffered) together with its column-LSE state, which makes one extra hop home at the end.
+// Backward is two symmetric passes: the dI pass keeps I stationary and
+// streams (T, c); the dT pass keeps T stationary and streams (I, r).  Gradients therefore never travel.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "host_utils.h"
+#include "kernels.h"
+
+using namespace infcl;
+
+// ------------------------------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+#define LOAD(name) api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, "nccl" #name))
+      LOAD(GetUniqueId);
+      LOAD(CommInitRank);
+      LOAD(CommDestroy);
+      LOAD(Send);
+      LOAD(Recv);
+      LOAD(GroupStart);
+      LOAD(GroupEnd);
+      LOAD(AllReduce);
+      LOAD(GetErrorString);
+#undef LOAD
+      api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.GroupStart &&
+               api.GroupEnd && api.AllReduce;
+    }
+  }
+  return api;
+}
+
+#define INFCL_NCCL_TRY(expr)                                                                                  \
+  do {                                                                                                        \
+    ncclResult_t _r = (expr);                                                                                 \
+    if (_r != ncclSuccess)                                                                                    \
+      return fail(INFCL_ERR_NCCL, std::string(#expr) + ": " +                                                 \
+                                      (nccl().GetErrorString ? nccl().GetErrorString(_r) : std::to_string(_r))); \
+  } while (0)
+}  // namespace
+
+struct infcl_comm_s {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1, device = 0;
+  cudaStream_t stream = nullptr;  // communication stream (NCCL P2P overlapped with compute)
+  std::vector<cudaEvent_t> ev;    // event pool
+};
+
+extern "C" infcl_status infcl_get_unique_id(void* id128) {
+  if (!id128) return fail(INFCL_ERR_INVALID_ARG, "null id buffer");
+  if (!nccl().ok) return fail(INFCL_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  INFCL_NCCL_TRY(nccl().GetUniqueId(&id));
+  std::memcpy(id128, &id, sizeof(id));
+  return INFCL_OK;
+}
+
+extern "C" infcl_status infcl_comm_init(infcl_comm* out, int rank, int world, const void* id128, int device) {
+  if (!out || !id128) return fail(INFCL_ERR_INVALID_ARG, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(INFCL_ERR_CONFIG, "rank out of range");
+  if (!nccl().ok) return fail(INFCL_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  INFCL_CUDA_TRY(cudaSetDevice(device));
+  auto* c = new infcl_comm_s();
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  ncclResult_t r = nccl().CommInitRank(&c->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(INFCL_ERR_NCCL, "ncclCommInitRank failed");
+  }
+  cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, -1);
+  c->ev.resize(8);
+  for (auto& e : c->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  *out = c;
+  return INFCL_OK;
+}
+
+extern "C" infcl_status infcl_comm_destroy(infcl_comm c) {
+  if (!c) return INFCL_OK;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->comm) nccl().CommDestroy(c->comm);
+  delete c;
+  return INFCL_OK;
+}
+
+// ------------------------------------------------------------------------------------------ workspace
+namespace {
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {
+  int bs = 0, d = 0, dk = 0, world = 1;
+  bool f32 = false;
+  PassGeom g{};
+  long long slot_ld = 0;
+  size_t off_slots, off_rparts, off_rstate, off_cstate, off_own2, off_ring_lse, off_ring_blk, off_expA, off_expB,
+      off_dscr, off_acc, total;
+};
+
+Layout make_layout(int64_t b, int d, int world, infcl_dtype dt) {
+  Layout L;
+  L.bs = (int)(b / world);
+  L.d = d;
+  L.world = world;
+  L.f32 = dt == INFCL_FP32;
+  L.dk = L.f32 ? 3 * d : d;
+  L.g = pass_geom(L.bs, L.bs);
+  L.slot_ld = (long long)L.g.n_ct * kColsPerTile;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += align_up(bytes);
+    return at;
+  };
+  L.off_slots = take((size_t)2 * L.g.npairs * L.slot_ld * sizeof(float2));
+  L.off_rparts = take((size_t)(L.g.n_rb + L.g.npairs) * kRowsPerPair * sizeof(float2));
+  L.off_rstate = take((size_t)L.bs * sizeof(float2));
+  L.off_cstate = take((size_t)3 * L.bs * sizeof(float2));
+  L.off_own2 = take((size_t)2 * L.bs * sizeof(float));
+  L.off_ring_lse = take(world > 1 ? (size_t)2 * L.bs * sizeof(float) : 0);
+  L.off_ring_blk = take(world > 1 ? (size_t)2 * L.bs * L.dk * 2 : 0);
+  L.off_expA = take(L.f32 ? (size_t)L.bs * L.dk * 2 : 0);
+  L.off_expB = take(L.f32 ? (size_t)L.bs * L.dk * 2 : 0);
+  L.off_dscr = take(L.f32 ? (size_t)L.bs * L.dk * sizeof(float) : 0);
+  L.off_acc = take(64);
+  L.total = o;
+  return L;
+}
+
+infcl_status validate(const void* I, const void* T, infcl_dtype dt, int64_t b, int d, float s, int rank, int world,
+                      const void* ws, size_t ws_bytes, size_t need) {
+  if (!I || !T) return fail(INFCL_ERR_INVALID_ARG, "null feature pointer");
+  if (dt != INFCL_BF16 && dt != INFCL_FP32) return fail(INFCL_ERR_INVALID_ARG, "bad dtype");
+  if (!std::isfinite(s) || s < 0.f) return fail(INFCL_ERR_INVALID_ARG, "logit scale must be finite and >= 0");
+  if (b < 1 || d < 1) return fail(INFCL_ERR_SHAPE, "b and d must be >= 1");
+  if (d % 8) return fail(INFCL_ERR_SHAPE, "d must be a multiple of 8 (16-byte TMA rows)");
+  if ((dt == INFCL_BF16 && d > kMaxD) || (dt == INFCL_FP32 && 3 * d > kMaxD))
+    return fail(INFCL_ERR_SHAPE, "d=" + std::to_string(d) + " above the kernel limit (768 bf16, 256 fp32)");
+  if (world < 1 || rank < 0 || rank >= world) return fail(INFCL_ERR_CONFIG, "rank out of range");
+  if (b % world)
+    return fail(INFCL_ERR_CONFIG, "b=" + std::to_string(b) + " not divisible by world=" + std::to_string(world));
+  if (b / world > (int64_t)1 << 30) return fail(INFCL_ERR_SHAPE, "per-rank batch too large");
+  if (!ws || ws_bytes < need)
+    return fail(INFCL_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+  if ((reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return fail(INFCL_ERR_WORKSPACE, "workspace not 256-B aligned");
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(INFCL_ERR_UNSUPPORTED, "no CUDA device");
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) return fail(INFCL_ERR_UNSUPPORTED, "device is not sm_100 (B200)");
+  return INFCL_OK;
+}
+
+// Per-rank view of the workspace and the rank's operands (expanded to bf16 K-width dk).
+struct Rank {
+  Layout L;
+  uint8_t* ws = nullptr;
+  const __nv_bfloat16* A = nullptr;  // image side I (or I' = [hi|hi|lo] for fp32)
+  const __nv_bfloat16* B = nullptr;  // text side  T (or T' = [hi|lo|hi])
+  const void* I_orig = nullptr;
+  const void* T_orig = nullptr;
+  float s = 0.f;
+  int64_t b = 0;
+  float2* slots() const { return reinterpret_cast<float2*>(ws + L.off_slots); }
+  float2* rparts() const { return reinterpret_cast<float2*>(ws + L.off_rparts); }
+  float2* rstate() const { return reinterpret_cast<float2*>(ws + L.off_rstate); }
+  float2* cstate(int i) const { return reinterpret_cast<float2*>(ws + L.off_cstate) + (size_t)i * L.bs; }
+  float* own2(int i) const { return reinterpret_cast<float*>(ws + L.off_own2) + (size_t)i * L.bs; }
+  float* ring_lse(int i) const { return reinterpret_cast<float*>(ws + L.off_ring_lse) + (size_t)i * L.bs; }
+  __nv_bfloat16* ring_blk(int i) const {
+    return reinterpret_cast<__nv_bfloat16*>(ws + L.off_ring_blk) + (size_t)i * L.bs * L.dk;
+  }
+  float* dscr() const { return reinterpret_cast<float*>(ws + L.off_dscr); }
+  double* acc() const { return reinterpret_cast<double*>(ws + L.off_acc); }
+};
+
+infcl_status prepare_rank(Rank& R, const void* I, const void* T, infcl_dtype dt, int64_t b, int d, float s, int world,
+                          void* ws, cudaStream_t st) {
+  R.L = make_layout(b, d, world, dt);
+  R.ws = static_cast<uint8_t*>(ws);
+  R.s = s;
+  R.b = b;
+  R.I_orig = I;
+  R.T_orig = T;
+  if (dt == INFCL_FP32) {
+    auto* eA = reinterpret_cast<__nv_bfloat16*>(R.ws + R.L.off_expA);
+    auto* eB = reinterpret_cast<__nv_bfloat16*>(R.ws + R.L.off_expB);
+    launch_split_f32(static_cast<const float*>(I), eA, R.L.bs, d, 0, st);
+    launch_split_f32(static_cast<const float*>(T), eB, R.L.bs, d, 1, st);
+    R.A = eA;
+    R.B = eB;
+  } else {
+    R.A = static_cast<const __nv_bfloat16*>(I);
+    R.B = static_cast<const __nv_bfloat16*>(T);
+  }
+  INFCL_CUDA_TRY(cudaGetLastError());
+  return INFCL_OK;
+}
+
+// ---- forward pieces
+infcl_status fwd_begin(Rank& R, cudaStream_t st) {
+  launch_init_state(R.rstate(), R.L.bs, st);
+  launch_init_state(R.cstate(0), R.L.bs, st);
+  return INFCL_OK;
+}
+
+// main kernel of one ring step: stationary rows A vs held block; then fold row partials
+infcl_status fwd_step_main(Rank& R, const __nv_bfloat16* held, bool own, float* diag, cudaStream_t st) {
+  PassArgs a{};
+  a.A = R.A;
+  a.B = held;
+  a.nrows = a.ncols = R.L.bs;
+  a.dk = a.ld = R.L.dk;
+  a.scale = R.s;
+  a.diag_on = own ? 1 : 0;
+  a.col_slots = R.slots();
+  a.slot_ld = R.L.slot_ld;
+  a.row_parts = R.rparts();
+  a.diag_out = own ? diag : nullptr;
+  infcl_status s = launch_pair_forward(a, st);
+  if (s) return s;
+  launch_merge_rows(R.rparts(), R.rstate(), R.L.bs, R.L.g, st);
+  return INFCL_OK;
+}
+
+void fwd_step_cols(Rank& R, float2* held_cstate, cudaStream_t st) {
+  launch_merge_cols(R.slots(), R.L.slot_ld, held_cstate, R.L.bs, R.L.g, st);
+}
+
+void fwd_finish(Rank& R, const float2* own_cstate, float* row_lse, float* col_lse, const float* diag, double* acc,
+                cudaStream_t st) {
+  launch_finalize_lse(R.rstate(), row_lse, nullptr, R.L.bs, st);
+  launch_finalize_lse(own_cstate, col_lse, nullptr, R.L.bs, st);
+  launch_loss_partial(row_lse, col_lse, diag, R.L.bs, acc, st);
+}
+
+// ---- backward pieces
+infcl_status bwd_step(Rank& R, const __nv_bfloat16* rowsA, const float* lse_rows2, const __nv_bfloat16* held,
+                      const float* lse_cols2, bool own, float* dst, int ld_dst, const float* grad, cudaStream_t st) {
+  PassArgs a{};
+  a.A = rowsA;
+  a.B = held;
+  a.nrows = a.ncols = R.L.bs;
+  a.dk = a.ld = R.L.dk;
+  a.scale = R.s;
+  a.diag_on = own ? 1 : 0;
+  a.lse_row2 = lse_rows2;
+  a.lse_col2 = lse_cols2;
+  a.dA = dst;
+  a.ld_dA = ld_dst;
+  a.d_out = R.L.dk;
+  a.grad = grad;
+  a.coef_base = (float)((double)R.s / (2.0 * (double)R.b));
+  return launch_pair_backward(a, st);
+}
+
+infcl_status bwd_begin(Rank& R, const float* row_lse, const float* col_lse, float* dI, float* dT, cudaStream_t st) {
+  launch_scale_log2(row_lse, R.own2(0), R.L.bs, st);
+  launch_scale_log2(col_lse, R.own2(1), R.L.bs, st);
+  if (R.L.f32) {
+    INFCL_CUDA_TRY(cudaMemsetAsync(R.dscr(), 0, (size_t)R.L.bs * R.L.dk * sizeof(float), st));
+  } else {
+    INFCL_CUDA_TRY(cudaMemsetAsync(dI, 0, (size_t)R.L.bs * R.L.d * sizeof(float), st));
+  }
+  (void)dT;
+  return INFCL_OK;
+}
+
+// dst of pass 0 (dI) / pass 1 (dT): fp32 mode accumulates into the 3d-wide scratch then combines
+float* pass_dst(Rank& R, float* out) { return R.L.f32 ? R.dscr() : out; }
+
+infcl_status pass_end(Rank& R, int pass, float* out, const float* diag, const float* row_lse, const float* col_lse,
+                      const float* grad, cudaStream_t st) {
+  // pass 0 (dI): B_i = T_i; pass 1 (dT): B_i = I_i
+  if (R.L.f32) {
+    launch_combine_f32(R.dscr(), R.L.dk, out, R.L.bs, R.L.d, pass == 0 ? 0 : 1, st);
+  }
+  const void* Bi = pass == 0 ? R.T_orig : R.I_orig;
+  launch_diag_correction(out, R.L.d, Bi, R.L.d, R.L.f32 ? 1 : 0, diag, row_lse, col_lse, grad,
+                         (float)((double)R.s / (2.0 * (double)R.b)), R.s, R.L.bs, R.L.d, st);
+  if (pass == 0) {
+    if (R.L.f32) {
+      INFCL_CUDA_TRY(cudaMemsetAsync(R.dscr(), 0, (size_t)R.L.bs * R.L.dk * sizeof(float), st));
+    }
+  }
+  INFCL_CUDA_TRY(cudaGetLastError());
+  return INFCL_OK;
+}
+
+cudaEvent_t ev(infcl_comm c, int i) { return c->ev[i % c->ev.size()]; }
+
+int prev_rank(int r, int n) { return (r - 1 + n) % n; }
+int next_rank(int r, int n) { return (r + 1) % n; }
+
+// grouped send(to r-1) / recv(from r+1) of one buffer pair on the comm stream
+infcl_status ring_exchange(infcl_comm c, const void* send, void* recv, size_t bytes) {
+  const int n = c->world, r = c->rank;
+  INFCL_NCCL_TRY(nccl().GroupStart());
+  INFCL_NCCL_TRY(nccl().Send(send, bytes, ncclUint8, prev_rank(r, n), c->comm, c->stream));
+  INFCL_NCCL_TRY(nccl().Recv(recv, bytes, ncclUint8, next_rank(r, n), c->comm, c->stream));
+  INFCL_NCCL_TRY(nccl().GroupEnd());
+  return INFCL_OK;
+}
+}  // namespace
+
+extern "C" size_t infcl_workspace_bytes(int64_t b, int d, int world, infcl_dtype dt) {
+  if (b < 1 || d < 1 || world < 1 || b % world) return 0;
+  return make_layout(b, d, world, dt).total;
+}
+
+#define TRY(x)                      \
+  do {                              \
+    infcl_status _s = (x);          \
+    if (_s != INFCL_OK) return _s;  \
+  } while (0)
+
+extern "C" infcl_status infcl_forward(infcl_comm comm, const void* I_local, const void* T_local, infcl_dtype dt,
+                                      int64_t b, int d, float s, int rank, int world, float* row_lse, float* col_lse,
+                                      float* diag, float* loss, void* ws, size_t ws_bytes, void* stream) {
+  const size_t need = infcl_workspace_bytes(b, d, world, dt);
+  TRY(validate(I_local, T_local, dt, b, d, s, rank, world, ws, ws_bytes, need));
+  if (!row_lse || !col_lse || !diag || !loss) return fail(INFCL_ERR_INVALID_ARG, "null output pointer");
+  if (world > 1 && (!comm || comm->world != world || comm->rank != rank))
+    return fail(INFCL_ERR_CONFIG, "world > 1 needs a communicator with matching rank/world");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Rank R;
+  TRY(prepare_rank(R, I_local, T_local, dt, b, d, s, world, ws, st));
+  INFCL_CUDA_TRY(cudaMemsetAsync(R.acc(), 0, sizeof(double), st));
+  TRY(fwd_begin(R, st));
+  if (world == 1) {
+    TRY(fwd_step_main(R, R.B, true, diag, st));
+    fwd_step_cols(R, R.cstate(0), st);
+    fwd_finish(R, R.cstate(0), row_lse, col_lse, diag, R.acc(), st);
+    launch_loss_write(R.acc(), loss, b, st);
+    INFCL_CUDA_TRY(cudaGetLastError());
+    return INFCL_OK;
+  }
+  // ---- ring over `world` GPUs (Alg.1): T block prefetched one step ahead; column state follows compute
+  const size_t blk_bytes = (size_t)R.L.bs * R.L.dk * 2, cs_bytes = (size_t)R.L.bs * sizeof(float2);
+  const __nv_bfloat16* held = R.B;
+  INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 0), st));
+  INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 0), 0));  // inputs ready before the first send
+  for (int k = 0; k < world; ++k) {
+    __nv_bfloat16* next = R.ring_blk(k & 1);
+    if (k + 1 < world) {
+      TRY(ring_exchange(comm, held, next, blk_bytes));  // prefetch the block held at step k+1
+      INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 2), comm->stream));
+    }
+    TRY(fwd_step_main(R, held, k == 0, diag, st));
+    if (k >= 1) INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 3), 0));  // held block's column state arrived
+    float2* cs = R.cstate(k & 1);
+    fwd_step_cols(R, cs, st);
+    INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 1), st));  // compute of step k done
+    INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 1), 0));
+    TRY(ring_exchange(comm, cs, R.cstate((k + 1) & 1), cs_bytes));  // column state (last: return hop home)
+    INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 3), comm->stream));
+    if (k + 1 < world) INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 2), 0));  // next block arrived
+    held = next;
+  }
+  INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 3), 0));  // own column state is home
+  fwd_finish(R, R.cstate(world & 1), row_lse, col_lse, diag, R.acc(), st);
+  INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 4), st));
+  INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 4), 0));
+  INFCL_NCCL_TRY(nccl().AllReduce(R.acc(), R.acc(), 1, ncclFloat64, ncclSum, comm->comm, comm->stream));
+  INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 7), comm->stream));
+  INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 7), 0));
+  launch_loss_write(R.acc(), loss, b, st);
+  INFCL_CUDA_TRY(cudaGetLastError());
+  return INFCL_OK;
+}
+
+extern "C" infcl_status infcl_backward(infcl_comm comm, const void* I_local, const void* T_local, infcl_dtype dt,
+                                       int64_t b, int d, float s, int rank, int world, const float* row_lse,
+                                       const float* col_lse, const float* diag, const float* grad, float* dI,
+                                       float* dT, void* ws, size_t ws_bytes, void* stream) {
+  const size_t need = infcl_workspace_bytes(b, d, world, dt);
+  TRY(validate(I_local, T_local, dt, b, d, s, rank, world, ws, ws_bytes, need));
+  if (!row_lse || !col_lse || !diag || !grad || !dI || !dT) return fail(INFCL_ERR_INVALID_ARG, "null pointer");
+  if (world > 1 && (!comm || comm->world != world || comm->rank != rank))
+    return fail(INFCL_ERR_CONFIG, "world > 1 needs a communicator with matching rank/world");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Rank R;
+  TRY(prepare_rank(R, I_local, T_local, dt, b, d, s, world, ws, st));
+  TRY(bwd_begin(R, row_lse, col_lse, dI, dT, st));
+  const size_t blk_bytes = (size_t)R.L.bs * R.L.dk * 2, lse_bytes = (size_t)R.L.bs * sizeof(float);
+  for (int pass = 0; pass < 2; ++pass) {
+    // pass 0: rows I (lse r), stream (T, c) -> dI;  pass 1: rows T (lse c), stream (I, r) -> dT
+    const __nv_bfloat16* rows = pass == 0 ? R.A : R.B;
+    const __nv_bfloat16* own_blk = pass == 0 ? R.B : R.A;
+    const float* rows2 = R.own2(pass == 0 ? 0 : 1);
+    const float* own_cols2 = R.own2(pass == 0 ? 1 : 0);
+    float* out = pass == 0 ? dI : dT;
+    float* dst = pass_dst(R, out);
+    const int ld_dst = R.L.f32 ? R.L.dk : R.L.d;
+    if (!R.L.f32 && pass == 1) INFCL_CUDA_TRY(cudaMemsetAsync(dT, 0, (size_t)R.L.bs * R.L.d * sizeof(float), st));
+    if (world == 1) {
+      TRY(bwd_step(R, rows, rows2, own_blk, own_cols2, true, dst, ld_dst, grad, st));
+    } else {
+      const __nv_bfloat16* held = own_blk;
+      const float* held2 = own_cols2;
+      INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 0), st));
+      INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 0), 0));
+      for (int k = 0; k < world; ++k) {
+        __nv_bfloat16* next = R.ring_blk(k & 1);
+        float* next2 = R.ring_lse(k & 1);
+        if (k + 1 < world) {
+          if (k >= 1) {  // `next` was held at step k-1: its compute must be done before we overwrite it
+            INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 5 + ((k - 1) & 1)), 0));
+          }
+          TRY(ring_exchange(comm, held, next, blk_bytes));
+          TRY(ring_exchange(comm, held2, next2, lse_bytes));
+          INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 2), comm->stream));
+        }
+        TRY(bwd_step(R, rows, rows2, held, held2, k == 0, dst, ld_dst, grad, st));
+        INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 5 + (k & 1)), st));
+        if (k + 1 < world) INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 2), 0));
+        held = next;
+        held2 = next2;
+      }
+    }
+    TRY(pass_end(R, pass, out, diag, row_lse, col_lse, grad, st));
+  }
+  INFCL_CUDA_TRY(cudaGetLastError());
+  return INFCL_OK;
+}
+
+// ------------------------------------------------------------------------------------------ virtual ring
+// `world` logical ranks on one device, lock-step, blocks exchanged by device copies on the same stream.
+extern "C" infcl_status infcl_forward_virtual(const void* I, const void* T, infcl_dtype dt, int64_t b, int d, float s,
+                                              int world, float* row_lse, float* col_lse, float* diag, float* loss,
+                                              void* ws, size_t ws_bytes, void* stream) {
+  const size_t per = infcl_workspace_bytes(b, d, world, dt);
+  TRY(validate(I, T, dt, b, d, s, 0, world, ws, ws_bytes, per * (size_t)world));
+  if (!row_lse || !col_lse || !diag || !loss) return fail(INFCL_ERR_INVALID_ARG, "null output pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int bs = (int)(b / world);
+  const size_t esz = dt == INFCL_FP32 ? 4 : 2;
+  std::vector<Rank> R(world);
+  for (int r = 0; r < world; ++r) {
+    TRY(prepare_rank(R[r], static_cast<const uint8_t*>(I) + (size_t)r * bs * d * esz,
+                     static_cast<const uint8_t*>(T) + (size_t)r * bs * d * esz, dt, b, d, s, world,
+                     static_cast<uint8_t*>(ws) + (size_t)r * per, st));
+    INFCL_CUDA_TRY(cudaMemsetAsync(R[r].acc(), 0, sizeof(double), st));
+    TRY(fwd_begin(R[r], st));
+  }
+  const size_t blk_bytes = (size_t)bs * R[0].L.dk * 2, cs_bytes = (size_t)bs * sizeof(float2);
+  std::vector<const __nv_bfloat16*> held(world);
+  for (int r = 0; r < world; ++r) held[r] = R[r].B;
+  for (int k = 0; k < world; ++k) {
+    for (int r = 0; r < world; ++r) {
+      TRY(fwd_step_main(R[r], held[r], k == 0, diag + (size_t)r * bs, st));
+      fwd_step_cols(R[r], R[r].cstate(k & 1), st);
+    }
+    for (int r = 0; r < world; ++r) {  // rank r receives from r+1: block and column state
+      const int src = next_rank(r, world);
+      if (k + 1 < world)
+        INFCL_CUDA_TRY(cudaMemcpyAsync(R[r].ring_blk(k & 1), held[src], blk_bytes, cudaMemcpyDeviceToDevice, st));
+      INFCL_CUDA_TRY(cudaMemcpyAsync(R[r].cstate((k + 1) & 1) + 0, R[src].cstate(k & 1), cs_bytes,
+                                     cudaMemcpyDeviceToDevice, st));
+    }
+    for (int r = 0; r < world; ++r) held[r] = R[r].ring_blk(k & 1);
+  }
+  // every logical rank adds its partial into rank 0's accumulator (the virtual all-reduce)
+  for (int r = 0; r < world; ++r)
+    fwd_finish(R[r], R[r].cstate(world & 1), row_lse + (size_t)r * bs, col_lse + (size_t)r * bs,
+               diag + (size_t)r * bs, R[0].acc(), st);
+  launch_loss_write(R[0].acc(), loss, b, st);
+  INFCL_CUDA_TRY(cudaGetLastError());
+  return INFCL_OK;
+}
+
+extern "C" infcl_status infcl_backward_virtual(const void* I, const void* T, infcl_dtype dt, int64_t b, int d, float s,
+                                               int world, const float* row_lse, const float* col_lse,
+                                               const float* diag, const float* grad, float* dI, float* dT, void* ws,
+                                               size_t ws_bytes, void* stream) {
+  const size_t per = infcl_workspace_bytes(b, d, world, dt);
+  TRY(validate(I, T, dt, b, d, s, 0, world, ws, ws_bytes, per * (size_t)world));
+  if (!row_lse || !col_lse || !diag || !grad || !dI || !dT) return fail(INFCL_ERR_INVALID_ARG, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int bs = (int)(b / world);
+  const size_t esz = dt == INFCL_FP32 ? 4 : 2;
+  std::vector<Rank> R(world);
+  for (int r = 0; r < world; ++r) {
+    TRY(prepare_rank(R[r], static_cast<const uint8_t*>(I) + (size_t)r * bs * d * esz,
+                     static_cast<const uint8_t*>(T) + (size_t)r * bs * d * esz, dt, b, d, s, world,
+                     static_cast<uint8_t*>(ws) + (size_t)r * per, st));
+    TRY(bwd_begin(R[r], row_lse + (size_t)r * bs, col_lse + (size_t)r * bs, dI + (size_t)r * bs * d,
+                  dT + (size_t)r * bs * d, st));
+  }
+  const size_t blk_bytes = (size_t)bs * R[0].L.dk * 2, lse_bytes = (size_t)bs * sizeof(float);
+  for (int pass = 0; pass < 2; ++pass) {
+    std::vector<const __nv_bfloat16*> held(world);
+    std::vector<const float*> held2(world);
+    for (int r = 0; r < world; ++r) {
+      held[r] = pass == 0 ? R[r].B : R[r].A;
+      held2[r] = R[r].own2(pass == 0 ? 1 : 0);
+      if (!R[r].L.f32 && pass == 1)
+        INFCL_CUDA_TRY(cudaMemsetAsync(dT + (size_t)r * bs * d, 0, (size_t)bs * d * sizeof(float), st));
+    }
+    for (int k = 0; k < world; ++k) {
+      for (int r = 0; r < world; ++r) {
+        float* out = (pass == 0 ? dI : dT) + (size_t)r * bs * d;
+        TRY(bwd_step(R[r], pass == 0 ? R[r].A : R[r].B, R[r].own2(pass == 0 ? 0 : 1), held[r], held2[r], k == 0,
+                     pass_dst(R[r], out), R[r].L.f32 ? R[r].L.dk : d, grad, st));
+      }
+      if (k + 1 < world) {
+        for (int r = 0; r < world; ++r) {
+          const int src = next_rank(r, world);
+          INFCL_CUDA_TRY(cudaMemcpyAsync(R[r].ring_blk(k & 1), held[src], blk_bytes, cudaMemcpyDeviceToDevice, st));
+          INFCL_CUDA_TRY(cudaMemcpyAsync(R[r].ring_lse(k & 1), held2[src], lse_bytes, cudaMemcpyDeviceToDevice, st));
+        }
+        for (int r = 0; r < world; ++r) {
+          held[r] = R[r].ring_blk(k & 1);
+          held2[r] = R[r].ring_lse(k & 1);
+        }
+      }
+    }
+    for (int r = 0; r < world; ++r) {
+      float* out = (pass == 0 ? dI : dT) + (size_t)r * bs * d;
+      TRY(pass_end(R[r], pass, out, diag + (size_t)r * bs, row_lse + (size_t)r * bs, col_lse + (size_t)r * bs, grad,
+                   st));
+    }
+  }
+  INFCL_CUDA_TRY(cudaGetLastError());
+  return INFCL_OK;
+}
+
+// ------------------------------------------------------------------------------------------ e2e host entry
+extern "C" size_t infcl_e2e_scratch_bytes(int64_t b, int d, infcl_dtype dt) {
+  if (b < 1 || d < 1) return 0;
+  const size_t esz = dt == INFCL_FP32 ? 4 : 2;
+  size_t o = 0;
+  o += align_up((size_t)b * d * esz) * 2;          // I, T
+  o += align_up((size_t)b * sizeof(float)) * 3;    // r, c, diag
+  o += align_up(64);                               // loss, grad
+  o += align_up((size_t)b * d * sizeof(float)) * 2;  // dI, dT
+  o += infcl_workspace_bytes(b, d, 1, dt);
+  return o;
+}
+
+extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_host, infcl_dtype dt, int64_t b, int d,
+                                             float s, float grad_loss, float* loss_host, float* dI_host,
+                                             float* dT_host, void* scratch, size_t scratch_bytes, void* stream) {
+  if (!I_host || !T_host || !loss_host || !dI_host || !dT_host || !scratch)
+    return fail(INFCL_ERR_INVALID_ARG, "null pointer");
+  const size_t need = infcl_e2e_scratch_bytes(b, d, dt);
+  if (need == 0) return fail(INFCL_ERR_SHAPE, "bad shape");
+  if (scratch_bytes < need) return fail(INFCL_ERR_WORKSPACE, "scratch too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t esz = dt == INFCL_FP32 ? 4 : 2;
+  uint8_t* p = static_cast<uint8_t*>(scratch);
+  auto take = [&](size_t bytes) {
+    uint8_t* at = p;
+    p += align_up(bytes);
+    return at;
+  };
+  void* I = take((size_t)b * d * esz);
+  void* T = take((size_t)b * d * esz);
+  float* r = reinterpret_cast<float*>(take((size_t)b * 4));
+  float* c = reinterpret_cast<float*>(take((size_t)b * 4));
+  float* dg = reinterpret_cast<float*>(take((size_t)b * 4));
+  float* lg = reinterpret_cast<float*>(take(64));
+  float* dI = reinterpret_cast<float*>(take((size_t)b * d * 4));
+  float* dT = reinterpret_cast<float*>(take((size_t)b * d * 4));
+  void* ws = p;
+  const size_t wsb = infcl_workspace_bytes(b, d, 1, dt);
+  INFCL_CUDA_TRY(cudaMemcpyAsync(I, I_host, (size_t)b * d * esz, cudaMemcpyHostToDevice, st));
+  INFCL_CUDA_TRY(cudaMemcpyAsync(T, T_host, (size_t)b * d * esz, cudaMemcpyHostToDevice, st));
+  INFCL_CUDA_TRY(cudaMemcpyAsync(lg + 1, &grad_loss, sizeof(float), cudaMemcpyHostToDevice, st));
+  TRY(infcl_forward(nullptr, I, T, dt, b, d, s, 0, 1, r, c, dg, lg, ws, wsb, stream));
+  TRY(infcl_backward(nullptr, I, T, dt, b, d, s, 0, 1, r, c, dg, lg + 1, dI, dT, ws, wsb, stream));
+  INFCL_CUDA_TRY(cudaMemcpyAsync(loss_host, lg, sizeof(float), cudaMemcpyDeviceToHost, st));
+  INFCL_CUDA_TRY(cudaMemcpyAsync(dI_host, dI, (size_t)b * d * 4, cudaMemcpyDeviceToHost, st));
+  INFCL_CUDA_TRY(cudaMemcpyAsync(dT_host, dT, (size_t)b * d * 4, cudaMemcpyDeviceToHost, st));
+  INFCL_CUDA_TRY(cudaStreamSynchronize(st));
+  return INFCL_OK;
+}
+
+extern "C" uint64_t infcl_launch_count(void) { return launch_counter(); }
+extern "C" void infcl_reset_launch_count(void) { launch_counter() = 0; }

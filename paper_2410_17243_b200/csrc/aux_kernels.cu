@@ -1,0 +1,196 @@
+// Small O(b)-work kernels around the fused pair kernel: LSE state merges (Eq.4 with the -inf identity,
+// readings Q1/Q2, in the base-2 (m, sigma) form), LSE finalisation, the loss sum (Eq.2, fp64), the exact
+// fp32 diagonal gradient term (reading H7) and the fp32 hi/lo bf16 split.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "kernels.h"
+
+namespace infcl {
+
+uint64_t& launch_counter() {
+  static thread_local uint64_t n = 0;
+  return n;
+}
+
+static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+__device__ __forceinline__ float2 merge_ms(float2 a, float2 b) {
+  const float M = fmaxf(a.x, b.x);
+  if (M == -INFINITY) return make_float2(-INFINITY, 0.f);
+  return make_float2(M, a.y * exp2f(a.x - M) + b.y * exp2f(b.x - M));
+}
+
+__device__ __forceinline__ long long item_begin_h(long long n_items, int npairs, int p) {
+  return (long long)p * n_items / npairs;
+}
+
+__device__ int pair_of(long long item, long long n_items, int npairs) {
+  int p = (int)(((item + 1) * npairs + n_items - 1) / n_items) - 1;
+  p = max(0, min(npairs - 1, p));
+  while (p > 0 && item_begin_h(n_items, npairs, p) > item) --p;
+  while (p + 1 < npairs && item_begin_h(n_items, npairs, p + 1) <= item) ++p;
+  return p;
+}
+
+__global__ void init_state_kernel(float2* st, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) st[i] = make_float2(-INFINITY, 0.f);
+}
+
+__global__ void merge_rows_kernel(const float2* __restrict__ parts, float2* __restrict__ state, int nrows, int n_ct,
+                                  long long n_items, int npairs) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  const int rb = i / kRowsPerPair;
+  const int p0 = pair_of((long long)rb * n_ct, n_items, npairs);
+  const int p1 = pair_of((long long)(rb + 1) * n_ct - 1, n_items, npairs);
+  float2 acc = state[i];
+  for (int p = p0; p <= p1; ++p) acc = merge_ms(acc, parts[(long long)(p + rb) * kRowsPerPair + (i % kRowsPerPair)]);
+  state[i] = acc;
+}
+
+__global__ void merge_cols_kernel(const float2* __restrict__ slots, long long slot_ld, float2* __restrict__ state,
+                                  int ncols, int n_ct, long long n_items, int npairs) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  const int ct = j / kColsPerTile;
+  float2 acc = state[j];
+  for (int p = 0; p < npairs; ++p) {
+    const long long a = item_begin_h(n_items, npairs, p), e = item_begin_h(n_items, npairs, p + 1);
+    bool visited;
+    if (e - a >= n_ct) visited = true;
+    else if (e == a) visited = false;
+    else visited = a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e;
+    if (!visited) continue;
+    acc = merge_ms(acc, slots[(long long)(2 * p) * slot_ld + j]);
+    acc = merge_ms(acc, slots[(long long)(2 * p + 1) * slot_ld + j]);
+  }
+  state[j] = acc;
+}
+
+__global__ void finalize_lse_kernel(const float2* __restrict__ st, float* __restrict__ lse, float* __restrict__ lse2,
+                                    int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float2 s = st[i];
+  const float l2 = (s.x == -INFINITY) ? -INFINITY : s.x + log2f(s.y);
+  if (lse) lse[i] = l2 * 0.69314718055994531f;
+  if (lse2) lse2[i] = l2;
+}
+
+__global__ void loss_partial_kernel(const float* __restrict__ r, const float* __restrict__ c,
+                                    const float* __restrict__ diag, int n, double* acc) {
+  double v = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    v += (double)r[i] + (double)c[i] - 2.0 * (double)diag[i];
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __shared__ double ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) atomicAdd(acc, v);
+  }
+}
+
+__global__ void loss_write_kernel(const double* acc, float* loss, double inv2b) { *loss = (float)(*acc * inv2b); }
+
+__global__ void scale_log2_kernel(const float* __restrict__ x, float* __restrict__ y, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = x[i] * 1.4426950408889634f;
+}
+
+// dA_i += s * g/(2b) * (e^{x_ii - r_i} + e^{x_ii - c_i} - 2) * B_i   (exact fp32 diagonal term, H7)
+__global__ void diag_correction_kernel(float* __restrict__ dA, int ld_dA, const void* __restrict__ B, int ldB,
+                                       int b_f32, const float* __restrict__ diag, const float* __restrict__ r,
+                                       const float* __restrict__ c, const float* __restrict__ grad, float coef_base,
+                                       int n, int d) {
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  const float x = diag[i];
+  const float w = coef_base * grad[0] * (expf(x - r[i]) + expf(x - c[i]) - 2.f);
+  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+    float bv;
+    if (b_f32) bv = reinterpret_cast<const float*>(B)[(long long)i * ldB + k];
+    else bv = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B)[(long long)i * ldB + k]);
+    dA[(long long)i * ld_dA + k] += w * bv;
+  }
+}
+
+// fp32 -> [hi | hi | lo] (mode 0) or [hi | lo | hi] (mode 1) bf16 rows of width 3d: I'.T'^T = hi.hi + hi.lo + lo.hi
+__global__ void split_f32_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int n, int d,
+                                 int mode) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)n * d) return;
+  const long long i = idx / d;
+  const int k = (int)(idx % d);
+  const float v = x[idx];
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+  __nv_bfloat16* o = out + i * 3 * d;
+  o[k] = hi;
+  o[d + k] = mode == 0 ? hi : lo;
+  o[2 * d + k] = mode == 0 ? lo : hi;
+}
+
+// out = in[:, 0:d] + in[:, d:2d] (mode 0) or in[:, 0:d] + in[:, 2d:3d] (mode 1)
+__global__ void combine_f32_kernel(const float* __restrict__ in, int ld_in, float* __restrict__ out, int n, int d,
+                                   int mode) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)n * d) return;
+  const long long i = idx / d;
+  const int k = (int)(idx % d);
+  const float* row = in + i * ld_in;
+  out[idx] = row[k] + row[(mode == 0 ? d : 2 * d) + k];
+}
+
+void launch_init_state(float2* st, int n, cudaStream_t s) {
+  init_state_kernel<<<nblk(n, 256), 256, 0, s>>>(st, n);
+  ++launch_counter();
+}
+void launch_merge_rows(const float2* parts, float2* state, int nrows, const PassGeom& g, cudaStream_t s) {
+  merge_rows_kernel<<<nblk(nrows, 256), 256, 0, s>>>(parts, state, nrows, g.n_ct, g.n_items, g.npairs);
+  ++launch_counter();
+}
+void launch_merge_cols(const float2* slots, long long slot_ld, float2* state, int ncols, const PassGeom& g,
+                       cudaStream_t s) {
+  merge_cols_kernel<<<nblk(ncols, 256), 256, 0, s>>>(slots, slot_ld, state, ncols, g.n_ct, g.n_items, g.npairs);
+  ++launch_counter();
+}
+void launch_finalize_lse(const float2* st, float* lse, float* lse2, int n, cudaStream_t s) {
+  finalize_lse_kernel<<<nblk(n, 256), 256, 0, s>>>(st, lse, lse2, n);
+  ++launch_counter();
+}
+void launch_loss_partial(const float* r, const float* c, const float* diag, int n, double* acc, cudaStream_t s) {
+  loss_partial_kernel<<<std::min(nblk(n, 256), 296u), 256, 0, s>>>(r, c, diag, n, acc);
+  ++launch_counter();
+}
+void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s) {
+  loss_write_kernel<<<1, 1, 0, s>>>(acc, loss, 0.5 / (double)b);
+  ++launch_counter();
+}
+void launch_scale_log2(const float* x, float* y, int n, cudaStream_t s) {
+  scale_log2_kernel<<<nblk(n, 256), 256, 0, s>>>(x, y, n);
+  ++launch_counter();
+}
+void launch_diag_correction(float* dA, int ld_dA, const void* B, int ldB, int dtype_f32, const float* diag,
+                            const float* r, const float* c, const float* grad, float coef_base, float /*scale*/, int n,
+                            int d, cudaStream_t s) {
+  if (n <= 0) return;
+  diag_correction_kernel<<<n, 256, 0, s>>>(dA, ld_dA, B, ldB, dtype_f32, diag, r, c, grad, coef_base, n, d);
+  ++launch_counter();
+}
+void launch_split_f32(const float* x, void* out, int n, int d, int mode, cudaStream_t s) {
+  split_f32_kernel<<<nblk((long long)n * d, 256), 256, 0, s>>>(x, reinterpret_cast<__nv_bfloat16*>(out), n, d, mode);
+  ++launch_counter();
+}
+void launch_combine_f32(const float* in, int ld_in, float* out, int n, int d, int mode, cudaStream_t s) {
+  combine_f32_kernel<<<nblk((long long)n * d, 256), 256, 0, s>>>(in, ld_in, out, n, d, mode);
+  ++launch_counter();
+}
+
+}  // namespace infcl

@@ -1,0 +1,64 @@
+// Internal (C++) interface between the ABI layer (api.cu) and the CUDA kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/infcl.h"
+
+namespace infcl {
+
+constexpr int kRowsPerPair = 128;  // stationary rows per CTA pair (64 per SM)
+constexpr int kColsPerTile = 256;  // streamed columns per tile (128 per SM)
+constexpr int kMaxD = 768;         // TMEM budget: 128 (S) + 3 x 128 (dA^T chunks) columns
+
+// One "pass" of the pair kernel over (stationary A rows) x (streamed B block).
+struct PassArgs {
+  const void* A;        // [nrows][ld] bf16 stationary side (I for fwd / dI pass, T for the dT pass)
+  const void* B;        // [ncols][ld] bf16 streamed block
+  int nrows, ncols;     // valid rows of A and B
+  int dk, ld;           // K extent (feature dim) and row stride in elements
+  float scale;          // s
+  int diag_on;          // B is A's own block: the positive pair of row i is column i
+  // forward outputs (per pass / ring step)
+  float2* col_slots;    // [2 * npairs][slot_ld] (m2, sigma) partials (workspace)
+  long long slot_ld;
+  float2* row_parts;    // [(n_rb + npairs) * 128] row partials (workspace)
+  float* diag_out;      // [nrows] x_ii (natural units) or nullptr
+  // backward
+  const float* lse_row2;  // [nrows] row LSE in log2 units (r * log2 e)
+  const float* lse_col2;  // [ncols] column LSE in log2 units
+  float* dA;              // [nrows][ld_dA] fp32, accumulated with red.add
+  int ld_dA, d_out;
+  const float* grad;      // device scalar g
+  float coef_base;        // s / (2 b)
+};
+
+struct PassGeom {
+  int n_rb, n_ct, npairs;
+  long long n_items;
+};
+
+PassGeom pass_geom(int nrows, int ncols);
+infcl_status launch_pair_forward(const PassArgs& a, cudaStream_t s);
+infcl_status launch_pair_backward(const PassArgs& a, cudaStream_t s);
+
+// auxiliary kernels (aux_kernels.cu)
+void launch_init_state(float2* st, int n, cudaStream_t s);
+void launch_merge_rows(const float2* row_parts, float2* row_state, int nrows, const PassGeom& g, cudaStream_t s);
+void launch_merge_cols(const float2* col_slots, long long slot_ld, float2* col_state, int ncols, const PassGeom& g,
+                       cudaStream_t s);
+void launch_finalize_lse(const float2* st, float* lse, float* lse2, int n, cudaStream_t s);
+void launch_loss_partial(const float* r, const float* c, const float* diag, int n, double* acc, cudaStream_t s);
+void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s);
+void launch_scale_log2(const float* x, float* y, int n, cudaStream_t s);
+void launch_diag_correction(float* dA, int ld_dA, const void* B, int ldB, int dtype_f32, const float* diag,
+                            const float* r, const float* c, const float* grad, float coef_base, float scale, int n,
+                            int d, cudaStream_t s);
+void launch_split_f32(const float* x, void* out_bf16, int n, int d, int mode, cudaStream_t s);
+void launch_combine_f32(const float* in, int ld_in, float* out, int n, int d, int mode, cudaStream_t s);
+
+uint64_t& launch_counter();
+
+}  // namespace infcl

@@ -4,6 +4,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
+#include <cstdio>
 
 namespace infcl {
 
@@ -69,14 +70,30 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t pa
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// Deadlock watchdog: a wait that has not completed after ~2^35 cycles (~17 s) reports the barrier
+// (tag, block, thread, parity) and traps, so a protocol bug fails loudly instead of hanging the device.
+#ifndef INFCL_WATCHDOG_CYCLES
+#define INFCL_WATCHDOG_CYCLES (1ull << 35)
+#endif
+__device__ __noinline__ void watchdog_fire(int tag, uint32_t parity) {
+  printf("infcl watchdog: barrier tag=%d parity=%u stuck in block %d thread %d\n", tag, parity, (int)blockIdx.x,
+         (int)threadIdx.x);
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
   uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, parity)) return;
+  const unsigned long long t0 = clock64();
   while (!mbar_try_wait(a, parity)) {
+    if (clock64() - t0 > INFCL_WATCHDOG_CYCLES) watchdog_fire(tag, parity);
   }
 }
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity, int tag = 0) {
   uint32_t a = smem_u32(bar);
+  if (mbar_try_wait_cluster(a, parity)) return;
+  const unsigned long long t0 = clock64();
   while (!mbar_try_wait_cluster(a, parity)) {
+    if (clock64() - t0 > INFCL_WATCHDOG_CYCLES) watchdog_fire(tag, parity);
   }
 }
 

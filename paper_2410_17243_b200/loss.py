@@ -1,0 +1,180 @@
+"""Thin torch binding over the C ABI: device memory, streams and process groups only.
+
+Every step of the loss runs in libinfcl.so; this module allocates caller-owned buffers (so
+``torch.cuda.max_memory_allocated`` sees all of them), marshals pointers and the current stream, and wraps
+the pair forward/backward as an ``autograd.Function``.  The names mirror include/infcl.h.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib as L
+
+_DT = {torch.bfloat16: L.INFCL_BF16, torch.float32: L.INFCL_FP32}
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype not in _DT:
+        raise TypeError(f"features must be bf16 or fp32, got {t.dtype}")
+    return _DT[t.dtype]
+
+
+def _check_features(I: torch.Tensor, T: torch.Tensor):
+    if not (I.is_cuda and T.is_cuda):
+        raise ValueError("infcl: features must be CUDA tensors (there is no CPU path)")
+    if I.shape != T.shape or I.dim() != 2 or I.dtype != T.dtype:
+        raise ValueError(f"infcl: shape/dtype mismatch I{tuple(I.shape)} {I.dtype} T{tuple(T.shape)} {T.dtype}")
+    return I.contiguous(), T.contiguous()
+
+
+def workspace_bytes(b: int, d: int, world: int = 1, dtype=torch.bfloat16) -> int:
+    return int(L.lib().infcl_workspace_bytes(b, d, world, _DT[dtype]))
+
+
+def alloc_workspace(b: int, d: int, world: int, dtype, device, copies: int = 1) -> torch.Tensor:
+    n = workspace_bytes(b, d, world, dtype) * copies
+    return torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+
+
+class RingComm:
+    """NCCL ring communicator of the library, bootstrapped through torch.distributed (unique-id broadcast)."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        dev = torch.cuda.current_device() if device is None else device
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if self.rank == 0:
+            buf = (ctypes.c_uint8 * 128)()
+            L.call("infcl_get_unique_id", ctypes.cast(buf, ctypes.c_void_p))
+            uid = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            uid = uid.cuda()
+        dist.broadcast(uid, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        raw = bytes(uid.cpu().tolist())
+        idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(raw)
+        self.handle = ctypes.c_void_p()
+        L.call("infcl_comm_init", ctypes.byref(self.handle), self.rank, self.world, ctypes.cast(idbuf, ctypes.c_void_p),
+               dev)
+
+    def close(self):
+        if self.handle:
+            L.lib().infcl_comm_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def infcl_forward(I_local, T_local, b: int, logit_scale: float, rank: int = 0, world: int = 1, comm=None,
+                  workspace=None):
+    """Returns (loss scalar tensor, row_lse r, col_lse c, diag x_ii) for this rank's rows (include/infcl.h)."""
+    I_local, T_local = _check_features(I_local, T_local)
+    bs, d = I_local.shape
+    dev = I_local.device
+    r = torch.empty(bs, device=dev, dtype=torch.float32)
+    c = torch.empty_like(r)
+    dg = torch.empty_like(r)
+    loss = torch.empty((), device=dev, dtype=torch.float32)
+    ws = workspace if workspace is not None else alloc_workspace(b, d, world, I_local.dtype, dev)
+    L.call("infcl_forward", comm.handle if comm is not None else None, I_local.data_ptr(), T_local.data_ptr(),
+           _dtype_code(I_local), b, d, float(logit_scale), rank, world, r.data_ptr(), c.data_ptr(), dg.data_ptr(),
+           loss.data_ptr(), ws.data_ptr(), ws.numel(), _stream())
+    return loss, r, c, dg
+
+
+def infcl_backward(I_local, T_local, b: int, logit_scale: float, row_lse, col_lse, diag, grad_loss, rank: int = 0,
+                   world: int = 1, comm=None, workspace=None):
+    """Returns (dI, dT) fp32 for this rank's rows; grad_loss is a device scalar tensor."""
+    I_local, T_local = _check_features(I_local, T_local)
+    bs, d = I_local.shape
+    dev = I_local.device
+    dI = torch.empty(bs, d, device=dev, dtype=torch.float32)
+    dT = torch.empty_like(dI)
+    g = grad_loss.detach().to(device=dev, dtype=torch.float32).reshape(()).contiguous()
+    ws = workspace if workspace is not None else alloc_workspace(b, d, world, I_local.dtype, dev)
+    L.call("infcl_backward", comm.handle if comm is not None else None, I_local.data_ptr(), T_local.data_ptr(),
+           _dtype_code(I_local), b, d, float(logit_scale), rank, world, row_lse.data_ptr(), col_lse.data_ptr(),
+           diag.data_ptr(), g.data_ptr(), dI.data_ptr(), dT.data_ptr(), ws.data_ptr(), ws.numel(), _stream())
+    return dI, dT
+
+
+def infcl_forward_virtual(I, T, logit_scale: float, world: int):
+    """Whole batch on one device, ring schedule over `world` logical ranks (test of the ring engine)."""
+    I, T = _check_features(I, T)
+    b, d = I.shape
+    dev = I.device
+    r = torch.empty(b, device=dev, dtype=torch.float32)
+    c = torch.empty_like(r)
+    dg = torch.empty_like(r)
+    loss = torch.empty((), device=dev, dtype=torch.float32)
+    ws = alloc_workspace(b, d, world, I.dtype, dev, copies=world)
+    L.call("infcl_forward_virtual", I.data_ptr(), T.data_ptr(), _dtype_code(I), b, d, float(logit_scale), world,
+           r.data_ptr(), c.data_ptr(), dg.data_ptr(), loss.data_ptr(), ws.data_ptr(), ws.numel(), _stream())
+    return loss, r, c, dg
+
+
+def infcl_backward_virtual(I, T, logit_scale: float, world: int, r, c, dg, grad_loss):
+    I, T = _check_features(I, T)
+    b, d = I.shape
+    dev = I.device
+    dI = torch.empty(b, d, device=dev, dtype=torch.float32)
+    dT = torch.empty_like(dI)
+    g = grad_loss.detach().to(device=dev, dtype=torch.float32).reshape(()).contiguous()
+    ws = alloc_workspace(b, d, world, I.dtype, dev, copies=world)
+    L.call("infcl_backward_virtual", I.data_ptr(), T.data_ptr(), _dtype_code(I), b, d, float(logit_scale), world,
+           r.data_ptr(), c.data_ptr(), dg.data_ptr(), g.data_ptr(), dI.data_ptr(), dT.data_ptr(), ws.data_ptr(),
+           ws.numel(), _stream())
+    return dI, dT
+
+
+def infcl_loss_grad_host(I_host: torch.Tensor, T_host: torch.Tensor, logit_scale: float, grad_loss: float = 1.0,
+                         scratch: torch.Tensor | None = None):
+    """End-to-end call with HOST tensors (copies inside the library call); returns (loss, dI, dT) on host."""
+    b, d = I_host.shape
+    dt = _dtype_code(I_host)
+    n = int(L.lib().infcl_e2e_scratch_bytes(b, d, dt))
+    if scratch is None or scratch.numel() < n:
+        scratch = torch.empty(n, dtype=torch.uint8, device="cuda")
+    pin = I_host.is_pinned()
+    dI = torch.empty(b, d, dtype=torch.float32, pin_memory=pin)
+    dT = torch.empty_like(dI)
+    loss = torch.empty((), dtype=torch.float32)
+    L.call("infcl_loss_grad_host", I_host.data_ptr(), T_host.data_ptr(), dt, b, d, float(logit_scale),
+           float(grad_loss), loss.data_ptr(), dI.data_ptr(), dT.data_ptr(), scratch.data_ptr(), scratch.numel(),
+           _stream())
+    return loss, dI, dT
+
+
+class _InfCLFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, I_local, T_local, b, logit_scale, rank, world, comm):
+        loss, r, c, dg = infcl_forward(I_local, T_local, b, logit_scale, rank, world, comm)
+        ctx.save_for_backward(I_local, T_local, r, c, dg)
+        ctx.meta = (b, logit_scale, rank, world, comm)
+        return loss
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        I_local, T_local, r, c, dg = ctx.saved_tensors
+        b, s, rank, world, comm = ctx.meta
+        dI, dT = infcl_backward(I_local, T_local, b, s, r, c, dg, grad_out, rank, world, comm)
+        return dI.to(I_local.dtype), dT.to(T_local.dtype), None, None, None, None, None
+
+
+def infcl_loss(I_local: torch.Tensor, T_local: torch.Tensor, logit_scale: float, comm: RingComm | None = None):
+    """Symmetric InfoNCE loss L = (L_I + L_T)/2 over the global batch (this rank's shards), differentiable."""
+    world = comm.world if comm is not None else 1
+    rank = comm.rank if comm is not None else 0
+    b = I_local.shape[0] * world
+    return _InfCLFunction.apply(I_local, T_local, b, float(logit_scale), rank, world, comm)

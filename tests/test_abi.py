@@ -1,0 +1,62 @@
+"""CPU checks of the C ABI: the library loads without a GPU and exports every symbol include/infcl.h declares;
+host-only entry points behave; device entry points fail loudly (no CPU fallback)."""
+import ctypes
+import os
+import re
+
+from paper_2410_17243_b200 import _lib as L
+
+HEADER = os.path.join(os.path.dirname(__file__), "..", "include", "infcl.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(infcl_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    names = declared_symbols()
+    assert len(names) >= 15
+    lib = L.lib()
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in L.SIGNATURES, f"binding lacks {n}"
+    assert set(L.SIGNATURES) == set(names)
+
+
+def test_host_functions():
+    lib = L.lib()
+    assert lib.infcl_version() >= 100
+    assert lib.infcl_ring_block(2, 4, 2) == 0
+    assert lib.infcl_ring_block(0, 4, 4) == -1
+    for n in (1, 2, 3, 8, 16):
+        for step in range(n):
+            assert sorted(lib.infcl_ring_block(r, n, step) for r in range(n)) == list(range(n))
+    assert lib.infcl_status_string(3) == b"INFCL_ERR_CONFIG"
+    assert lib.infcl_workspace_bytes(7, 32, 2, 0) == 0  # b % world
+    assert lib.infcl_workspace_bytes(1024, 512, 1, 0) > 0
+
+
+def test_validation_errors_without_gpu():
+    lib = L.lib()
+    buf = ctypes.create_string_buffer(4096)
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    # b not divisible by world -> CONFIG, detected before touching any device
+    st = lib.infcl_forward(None, p, p, 0, 7, 32, 1.0, 0, 2, p, p, p, p, p, 4096, None)
+    assert st == 3 and b"divisible" in lib.infcl_last_error()
+    assert lib.infcl_forward(None, p, p, 0, 64, 30, 1.0, 0, 1, p, p, p, p, p, 4096, None) == 2  # d % 8
+    assert lib.infcl_forward(None, p, p, 0, 64, 32, float("inf"), 0, 1, p, p, p, p, p, 4096, None) == 1
+    assert lib.infcl_forward(None, None, p, 0, 64, 32, 1.0, 0, 1, p, p, p, p, p, 4096, None) == 1
+    # a valid call on a GPU-less host must fail (UNSUPPORTED or WORKSPACE), never silently succeed
+    assert lib.infcl_forward(None, p, p, 0, 64, 32, 1.0, 0, 1, p, p, p, p, p, 1 << 40, None) != 0
+
+
+def test_product_path_does_not_import_oracle():
+    import paper_2410_17243_b200
+    pkg = os.path.dirname(paper_2410_17243_b200.__file__)
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(root, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f

@@ -1,0 +1,151 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded inputs.
+
+Gates (BASELINE.json north_star): loss relative error <= 1e-4; gradient normwise relative error <= 2e-3
+(absolute <= 1e-6 max(s,1)|g| when the reference gradient is zero); r, c max-abs error <= 2e-3.
+Sizes span several 128x256 tiles and ragged tails; the full-size cases follow the large-b protocol.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import make_features
+from paper_2410_17243_b200 import loss as K
+
+pytestmark = pytest.mark.gpu
+
+LOSS_RTOL = 1e-4
+GRAD_RTOL = 2e-3
+LSE_ATOL = 2e-3
+
+
+def rel_norm(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    nr = np.linalg.norm(ref)
+    return np.linalg.norm(got - ref) / nr if nr > 0 else np.linalg.norm(got - ref)
+
+
+def check_all(I, T, s, g=1.0, world=None, want_grads=True):
+    Id, Td = I.cuda(), T.cuda()
+    b = I.shape[0]
+    if world is None:
+        loss, r, c, dg = K.infcl_forward(Id, Td, b, s)
+    else:
+        loss, r, c, dg = K.infcl_forward_virtual(Id, Td, s, world)
+    ref = oracle.forward(I, T, s)
+    torch.cuda.synchronize()
+    assert np.isfinite(loss.item())
+    assert abs(loss.item() - ref["loss"]) <= LOSS_RTOL * max(abs(ref["loss"]), 1e-6), (loss.item(), ref["loss"])
+    assert np.abs(r.cpu().numpy() - ref["r"]).max() <= LSE_ATOL
+    assert np.abs(c.cpu().numpy() - ref["c"]).max() <= LSE_ATOL
+    assert np.abs(dg.cpu().numpy() - ref["diag"]).max() <= LSE_ATOL
+    if not want_grads:
+        return
+    gt = torch.tensor(g, device="cuda")
+    if world is None:
+        dI, dT = K.infcl_backward(Id, Td, b, s, r, c, dg, gt)
+    else:
+        dI, dT = K.infcl_backward_virtual(Id, Td, s, world, r, c, dg, gt)
+    rdI, rdT = oracle.backward(I, T, s, g, ref["r"], ref["c"])
+    torch.cuda.synchronize()
+    for got, want in ((dI, rdI), (dT, rdT)):
+        got = got.cpu().numpy()
+        assert np.isfinite(got).all()
+        if np.linalg.norm(want) > 1e-9:
+            assert rel_norm(got, want) <= GRAD_RTOL, rel_norm(got, want)
+        else:
+            assert np.abs(got).max() <= 1e-6 * max(s, 1.0) * abs(g)
+
+
+@pytest.mark.parametrize("b,d", [(64, 32), (256, 64), (300, 128), (1000, 512), (2048, 768), (777, 256)])
+@pytest.mark.parametrize("s", [1.0, 14.2857])
+def test_parity_independent(b, d, s):
+    I, T = make_features(b, d, seed=b + d)
+    check_all(I, T, s)
+
+
+@pytest.mark.parametrize("s", [0.0, 100.0])
+def test_parity_scales(s):
+    I, T = make_features(1024, 512, seed=5, dist="paired")
+    check_all(I, T, s)
+
+
+@pytest.mark.parametrize("b,d", [(4096, 512), (4096, 768)])
+def test_parity_paired_multi_tile(b, d):
+    I, T = make_features(b, d, seed=3, dist="paired")
+    check_all(I, T, 14.2857, g=0.5)
+
+
+def test_identical_features_log_b():
+    I, T = make_features(512, 64, seed=0, dist="identical")
+    check_all(I, T, 14.2857)
+
+
+def test_onehot_closed_form_gpu():
+    b, K_, d = 1024, 32, 64
+    I, T = make_features(b, d, dist="onehot", K=K_)
+    cf = oracle.onehot_closed_form(b, K_, d, 14.2857)
+    loss, r, c, dg = K.infcl_forward(I.cuda(), T.cuda(), b, 14.2857)
+    dI, dT = K.infcl_backward(I.cuda(), T.cuda(), b, 14.2857, r, c, dg, torch.tensor(1.0, device="cuda"))
+    assert abs(loss.item() - cf["loss"]) <= LOSS_RTOL * cf["loss"]
+    assert rel_norm(dI.cpu().numpy(), cf["dI"]) <= GRAD_RTOL
+    assert rel_norm(dT.cpu().numpy(), cf["dT"]) <= GRAD_RTOL
+
+
+def test_fp32_cfg1():
+    # BASELINE cfg1: b=64, d=32, fp32 (hi/lo bf16 split on the same tensor-core kernel)
+    I, T = make_features(64, 32, seed=1, dtype=torch.float32)
+    check_all(I, T, 14.2857)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_virtual_ring_matches(world):
+    I, T = make_features(1024, 256, seed=9)
+    check_all(I, T, 14.2857, world=world)
+
+
+def test_b1_and_tiny():
+    I, T = make_features(8, 16, seed=2)
+    check_all(I, T, 3.0)
+    I1, T1 = make_features(1, 8, seed=2)
+    loss, r, c, dg = K.infcl_forward(I1.cuda(), T1.cuda(), 1, 3.0)
+    assert abs(loss.item()) < 1e-6
+
+
+def test_autograd_function():
+    I, T = make_features(512, 128, seed=4)
+    Id = I.cuda().requires_grad_(True)
+    Td = T.cuda().requires_grad_(True)
+    loss = K.infcl_loss(Id, Td, 14.2857)
+    (2.0 * loss).backward()
+    rdI, rdT = oracle.backward(I, T, 14.2857, 2.0)
+    assert rel_norm(Id.grad.float().cpu().numpy(), rdI) < 1e-2  # bf16-rounded gradient
+    assert rel_norm(Td.grad.float().cpu().numpy(), rdT) < 1e-2
+
+
+def test_e2e_host_entry():
+    I, T = make_features(640, 128, seed=8)
+    loss, dI, dT = K.infcl_loss_grad_host(I, T, 14.2857)
+    ref = oracle.loss_and_grads(I, T, 14.2857)
+    assert abs(loss.item() - ref["loss"]) <= LOSS_RTOL * ref["loss"]
+    assert rel_norm(dI.numpy(), ref["dI"]) <= GRAD_RTOL and rel_norm(dT.numpy(), ref["dT"]) <= GRAD_RTOL
+
+
+def test_nan_propagates():
+    I, T = make_features(256, 64, seed=1)
+    I[3, 5] = float("nan")
+    loss, r, c, dg = K.infcl_forward(I.cuda(), T.cuda(), 256, 1.0)
+    assert math.isnan(loss.item())
+
+
+def test_errors():
+    from paper_2410_17243_b200._lib import InfclError
+    I, T = make_features(64, 30 + 2, seed=1)
+    with pytest.raises(InfclError):
+        K.infcl_forward(I[:, :30].contiguous().cuda(), T[:, :30].contiguous().cuda(), 64, 1.0)  # d % 8
+    I, T = make_features(64, 32, seed=1)
+    with pytest.raises(InfclError):
+        K.infcl_forward(I.cuda(), T.cuda(), 64, float("nan"))
