@@ -130,6 +130,13 @@ int infcl_ring_block(int rank, int world, int step);
 uint64_t infcl_launch_count(void);
 void infcl_reset_launch_count(void);
 
+/* Kernel timing for bench.py / diagnostics.  While enabled, every fused pair-kernel launch is bracketed by
+ * CUDA events on its launch stream (kind 0 = forward pair kernel, kind 1 = backward pair kernel).
+ * infcl_profile_read waits for the recorded events and returns the launch count and the summed device
+ * milliseconds since the last infcl_profile_enable(1).  Single-threaded use only. */
+void infcl_profile_enable(int on);
+infcl_status infcl_profile_read(int kind, int* launches, double* total_ms);
+
 /* ---------------------------------------------------------------------------------------------------
  * Probes (hardware self-test of the UMMA building blocks; used by tests/test_gpu_probe.py):
  * D = A * B^T for one tile, A [M][K] (a_mn_major=0) or stored as [K][M] (a_mn_major=1), B [N][K] bf16;

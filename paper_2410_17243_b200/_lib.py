@@ -41,6 +41,8 @@ SIGNATURES = {
     "infcl_ring_block": (_i, [_i, _i, _i]),
     "infcl_launch_count": (ctypes.c_uint64, []),
     "infcl_reset_launch_count": (None, []),
+    "infcl_profile_enable": (None, [_i]),
+    "infcl_profile_read": (_i, [_i, ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_double)]),
     "infcl_probe_umma": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _i, _p]),
 }
 

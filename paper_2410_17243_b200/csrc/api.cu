@@ -616,3 +616,8 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
 
 extern "C" uint64_t infcl_launch_count(void) { return launch_counter(); }
 extern "C" void infcl_reset_launch_count(void) { launch_counter() = 0; }
+
+extern "C" void infcl_profile_enable(int on) { profile_enable(on != 0); }
+extern "C" infcl_status infcl_profile_read(int kind, int* launches, double* total_ms) {
+  return profile_read(kind, launches, total_ms);
+}

@@ -60,5 +60,7 @@ void launch_split_f32(const float* x, void* out_bf16, int n, int d, int mode, cu
 void launch_combine_f32(const float* in, int ld_in, float* out, int n, int d, int mode, cudaStream_t s);
 
 uint64_t& launch_counter();
+void profile_enable(bool on);
+infcl_status profile_read(int kind, int* launches, double* total_ms);
 
 }  // namespace infcl

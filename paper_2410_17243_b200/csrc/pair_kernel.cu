@@ -19,12 +19,32 @@
 
 #include <algorithm>
 #include <cmath>
+#include <utility>
+#include <vector>
 
 #include "host_utils.h"
 #include "kernels.h"
 #include "ptx.cuh"
 
 namespace infcl {
+
+// ---- optional per-launch event timing (infcl_profile_*)
+struct ProfState {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[2];
+};
+static ProfState& prof() {
+  static ProfState p;
+  return p;
+}
+static void prof_clear() {
+  for (auto& v : prof().ev)
+    for (auto& e : v) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+  for (auto& v : prof().ev) v.clear();
+}
 
 constexpr int kThreads = 192;
 constexpr int kBox = 8192;     // one TMA box: 64 rows x 64 bf16 (128 B, SW128)
@@ -502,13 +522,42 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
 
   auto kern = pair_kernel<BWD>;
   INFCL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof().on) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
   kern<<<dim3(2 * g.npairs), dim3(kThreads), smem, s>>>(tmA, tmB, k);
   INFCL_CUDA_TRY(cudaGetLastError());
+  if (prof().on) {
+    cudaEventRecord(e1, s);
+    prof().ev[BWD ? 1 : 0].push_back({e0, e1});
+  }
   ++launch_counter();
   return INFCL_OK;
 }
 
 infcl_status launch_pair_forward(const PassArgs& a, cudaStream_t s) { return launch_pair<false>(a, s); }
+
+void profile_enable(bool on) {
+  prof_clear();
+  prof().on = on;
+}
+
+infcl_status profile_read(int kind, int* launches, double* total_ms) {
+  if (kind < 0 || kind > 1 || !launches || !total_ms) return fail(INFCL_ERR_INVALID_ARG, "bad profile query");
+  double t = 0;
+  for (auto& e : prof().ev[kind]) {
+    INFCL_CUDA_TRY(cudaEventSynchronize(e.second));
+    float ms = 0;
+    INFCL_CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
+    t += ms;
+  }
+  *launches = (int)prof().ev[kind].size();
+  *total_ms = t;
+  return INFCL_OK;
+}
 infcl_status launch_pair_backward(const PassArgs& a, cudaStream_t s) { return launch_pair<true>(a, s); }
 
 }  // namespace infcl

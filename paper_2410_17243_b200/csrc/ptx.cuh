@@ -75,7 +75,7 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t pa
 #ifndef INFCL_WATCHDOG_CYCLES
 #define INFCL_WATCHDOG_CYCLES (1ull << 35)
 #endif
-__device__ __noinline__ void watchdog_fire(int tag, uint32_t parity) {
+static __device__ __noinline__ void watchdog_fire(int tag, uint32_t parity) {
   printf("infcl watchdog: barrier tag=%d parity=%u stuck in block %d thread %d\n", tag, parity, (int)blockIdx.x,
          (int)threadIdx.x);
   __trap();
