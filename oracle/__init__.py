@@ -22,6 +22,7 @@ from .infonce import (  # noqa: F401
     tiled_lse_rows,
     forward,
     backward,
+    backward_abs,
     loss_and_grads,
     loss_only,
     streamed_forward,

@@ -161,6 +161,33 @@ def backward(I, T, s: float, g: float = 1.0, r=None, c=None, want_ds: bool = Fal
     return dI, dT
 
 
+def backward_abs(I, T, s: float, g: float = 1.0, r=None, c=None, chunk: int = 4096):
+    """Magnitude of the gradient summands: (|s| |G| |T|, |s| |G|^T |I|) elementwise, with G as in ``backward``.
+    Any evaluation that rounds G (or T, I) to a working precision with unit roundoff u has componentwise error
+    <= ~u * this bound (standard GEMM rounding analysis); it is the conditioning term of the gradient gate."""
+    I = to_f64(I)
+    T = to_f64(T)
+    s32 = _scale32(s)
+    b, d = I.shape
+    if r is None or c is None:
+        f = forward(I, T, s)
+        r, c = f["r"], f["c"]
+    r = np.asarray(r, dtype=np.float64)
+    c = np.asarray(c, dtype=np.float64)
+    aI = np.zeros((b, d))
+    aT = np.zeros((b, d))
+    for i0 in range(0, b, chunk):
+        i1 = min(b, i0 + chunk)
+        Xc = s32 * (I[i0:i1] @ T.T)
+        G = (g / (2.0 * b)) * (np.exp(Xc - r[i0:i1, None]) + np.exp(Xc - c[None, :]))
+        rows = np.arange(i0, i1)
+        G[rows - i0, rows] -= g / b
+        G = np.abs(G)
+        aI[i0:i1] = abs(s32) * (G @ np.abs(T))
+        aT += abs(s32) * (G.T @ np.abs(I[i0:i1]))
+    return aI, aT
+
+
 def loss_and_grads(I, T, s: float, g: float = 1.0) -> dict:
     f = forward(I, T, s)
     dI, dT = backward(I, T, s, g, f["r"], f["c"])

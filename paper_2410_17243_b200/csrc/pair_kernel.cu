@@ -12,8 +12,8 @@
 //              (d split across the pair: 128 d-rows per SM), N=128, K=256, B_C read MN-major from the same
 //              TMA tiles layout.  The dA accumulator stays in TMEM across the whole row block (Alg.4
 //              l.12 "dI += ..."), and is drained with red.add at the end of the row block.
-// Warp roles (192 threads): warp 0 TMA producer, warp 1 TMEM alloc + MMA issuer (leader CTA), warps 2-5
-// epilogue (TMEM lane quarter = warp % 4).
+// Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM alloc + MMA issuer (leader CTA), warps 2-9
+// epilogue (TMEM lane quarter = warp % 4, column slice = (warp - 2) / 4).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -46,7 +46,7 @@ static void prof_clear() {
   for (auto& v : prof().ev) v.clear();
 }
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr int kBox = 8192;     // one TMA box: 64 rows x 64 bf16 (128 B, SW128)
 constexpr int kStage = 16384;  // one ring stage: two boxes
 constexpr int kMaxStages = 12;
@@ -116,10 +116,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ __align__(8) uint64_t afull, afree, sfull[2], sfree[2], gready, gfree, dafull, dafree;
   __shared__ uint32_t tmem_base;
-  __shared__ __align__(16) float cmx[2][2][128];
-  __shared__ __align__(16) float csm[2][2][128];
-  __shared__ float2 rowx[64];
-  __shared__ __align__(16) float cval[2][256];
+  __shared__ __align__(16) float2 xch[4][2][64];  // forward column partials of the 2 warps of a group
+  __shared__ float2 rowx[4][64];                  // forward row partials of the 4 column slices
+  __shared__ __align__(16) float cval[2][256];    // backward column LSEs (log2), double-buffered
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = cluster_ctarank();
@@ -287,178 +286,231 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===================================================================== epilogue (both CTAs)
-    const int q = warp & 3;        // TMEM lane quarter
-    const int h = q >> 1;          // column half of the 256-column tile
-    const int rh = q & 1;          // which 32 of the CTA's 64 rows
+    // 8 warps: warp w reads TMEM lane quarter q = w % 4 (rows) and column slice u = (w - 2) / 4 of 64 columns.
+    // 2x2 layout of the S tile: quarter q -> rows 32*(q&1).., tile columns h*128 + u*64 + [0,64), h = q >> 1.
+    const int ep = warp - 2;
+    const int q = warp & 3;
+    const int u = ep >> 2;
+    const int h = q >> 1;
+    const int rh = q & 1;
     const int r = rh * 32 + lane;  // row within this CTA's 64
-    const int et = threadIdx.x - 64;
-    const uint32_t laddr = tbase + ((uint32_t)(q * 32) << 16);
+    const int grp = h * 2 + u;     // the 2 warps (rh = 0, 1) that share these 64 columns
+    const int et = ep * 32 + lane;  // 0..255
+    const uint32_t laddr = tbase + ((uint32_t)(q * 32) << 16) + u * 64;
     uint32_t sph[2] = {0, 0}, gfph = 0, daph = 0;
     int tile_ctr = 0;
     const float k2 = p.k2;
     float coef = 0.f;
-    if (BWD) coef = p.coef_base * __ldg(p.grad);
+    if (BWD) {
+      coef = p.coef_base * __ldg(p.grad);
+      if (it0 < it1) {  // column LSEs of the first tile (later tiles are prefetched one tile ahead)
+        const int j = (int)(it0 % p.n_ct) * kColsPerTile + et;
+        cval[0][et] = j < p.ncols ? __ldg(p.lse_col2 + j) : 0.f;
+      }
+    }
     long long it = it0;
     while (it < it1) {
       const int rb = (int)(it / p.n_ct);
       const long long seg_end = std::min<long long>(it1, (long long)(rb + 1) * p.n_ct);
       const int ig = rb * kRowsPerPair + (int)cta * 64 + r;
       const bool row_ok = ig < p.nrows;
-      float m = -INFINITY, sig = 0.f;
+      float m = -INFINITY, sig = 0.f;  // forward: running row state over this thread's column slice
       float r2 = 0.f;
       if (BWD && row_ok) r2 = __ldg(p.lse_row2 + ig);
       for (; it < seg_end; ++it) {
         const int ct = (int)(it % p.n_ct);
         const int buf = BWD ? 0 : (tile_ctr & 1);
-        const int cbase = ct * kColsPerTile + h * 128;  // global column of this thread's local column 0
-        float* cv = cval[tile_ctr & 1];
-        if (BWD) {
-          const int j0 = ct * kColsPerTile + et * 2;
-          cv[et * 2] = j0 < p.ncols ? __ldg(p.lse_col2 + j0) : 0.f;
-          cv[et * 2 + 1] = j0 + 1 < p.ncols ? __ldg(p.lse_col2 + j0 + 1) : 0.f;
+        const int cb = ct * kColsPerTile + h * 128 + u * 64;  // global column of this thread's column 0
+        const bool diag_tile = p.diag_on && ig >= cb && ig < cb + 64;
+        const bool clean = row_ok && (cb + 64 <= p.ncols) && !diag_tile;
+        float pre_c = 0.f;  // backward: next tile's column LSE (prefetch)
+        if (BWD && it + 1 < it1) {
+          const int j = (int)((it + 1) % p.n_ct) * kColsPerTile + et;
+          pre_c = j < p.ncols ? __ldg(p.lse_col2 + j) : 0.f;
+        }
+        float2 pre0 = make_float2(-INFINITY, 0.f), pre1 = pre0;  // forward: slot values (prefetch)
+        const bool first_visit = (it - it0) < p.n_ct;
+        float2* slot = p.col_slots + (long long)blockIdx.x * p.slot_ld;
+        if (!BWD && rh == 0 && !first_visit) {
+          if (cb + lane < p.ncols) pre0 = slot[cb + lane];
+          if (cb + 32 + lane < p.ncols) pre1 = slot[cb + 32 + lane];
         }
         mbar_wait(&sfull[buf], sph[buf], 8);
         sph[buf] ^= 1;
         tc_fence_after();
-        float v[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(laddr + buf * 128 + c * 32, v + c * 32);
+        float v[64];
+        tmem_ld32(laddr + buf * 128, v);
+        tmem_ld32(laddr + buf * 128 + 32, v + 32);
         tmem_ld_wait();
-        tc_fence_before();
-        named_bar_sync(1, 128);
-        if (et == 0) mbar_arrive_cluster(&sfree[buf], 0);
-        const bool diag_tile = p.diag_on && ig >= cbase && ig < cbase + 128;
+        if constexpr (BWD) {  // single S buffer: release it as soon as it is in registers
+          tc_fence_before();
+          named_bar_sync(1, 256);
+          if (et == 0) mbar_arrive_cluster(&sfree[buf], 0);
+        }
 
         if constexpr (!BWD) {
           // ---------------------------------------------------------- forward statistics
           if (diag_tile && row_ok && p.diag_out) {
             float dv = 0.f;
 #pragma unroll
-            for (int j = 0; j < 128; ++j) dv = (cbase + j == ig) ? v[j] : dv;
+            for (int j = 0; j < 64; ++j) dv = (cb + j == ig) ? v[j] : dv;
             p.diag_out[ig] = dv * p.scale;
           }
           float mt = -INFINITY;
 #pragma unroll
-          for (int j = 0; j < 128; ++j) {
-            const bool ok = row_ok && (cbase + j < p.ncols);
-            v[j] = ok ? v[j] * k2 : -INFINITY;
+          for (int j = 0; j < 64; ++j) {
+            v[j] *= k2;
             mt = fmaxf(mt, v[j]);
           }
-          const float mn = fmaxf(m, mt);
-          if (mn != -INFINITY) {
-            float acc = 0.f;
+          if (!(row_ok && cb + 64 <= p.ncols)) {  // ragged tile: mask columns / invalid row
+            mt = -INFINITY;
 #pragma unroll
-            for (int j = 0; j < 128; ++j) acc += ex2(v[j] - mn);
-            sig = sig * ex2(m - mn) + acc;
+            for (int j = 0; j < 64; ++j) {
+              v[j] = (row_ok && cb + j < p.ncols) ? v[j] : -INFINITY;
+              mt = fmaxf(mt, v[j]);
+            }
+          }
+          // shared exponentials: E_j = 2^{y_j - mt} serves the row sum and (weighted) the column sums
+          float acc = 0.f;
+          if (mt != -INFINITY) {
+#pragma unroll
+            for (int j = 0; j < 64; ++j) {
+              v[j] = ex2(v[j] - mt);
+              acc += v[j];
+            }
+            const float mn = fmaxf(m, mt);
+            sig = sig * ex2(m - mn) + acc * ex2(mt - mn);
             m = mn;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 64; ++j) v[j] = 0.f;
           }
-          // column max over this warp's 32 rows -> lane l holds column 32c + l
-          float cmax[4];
+          float Rw = mt;  // tile-local reference of this warp's 32 rows
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float t[32];
+          for (int o = 16; o; o >>= 1) Rw = fmaxf(Rw, __shfl_xor_sync(0xffffffffu, Rw, o));
+          const float w = (mt == -INFINITY) ? 0.f : ex2(mt - Rw);
+          float t[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) t[i] = v[c * 32 + i];
-            cmax[c] = xreduce32<true>(t, lane);
-          }
+          for (int i = 0; i < 32; ++i) t[i] = v[i] * w;
+          float S0 = xreduce32<false>(t, lane);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) cmx[h][rh][c * 32 + lane] = cmax[c];
-          named_bar_sync(2 + h, 64);
-          float csum[4];
+          for (int i = 0; i < 32; ++i) t[i] = v[32 + i] * w;
+          float S1 = xreduce32<false>(t, lane);
+          float m0 = Rw, m1 = Rw;
+          const bool bad = Rw != -INFINITY && ((cb + lane < p.ncols && S0 < 8.6736174e-19f) ||
+                                               (cb + 32 + lane < p.ncols && S1 < 8.6736174e-19f));  // < 2^-60
+          if (__any_sync(0xffffffffu, bad)) {
+            // exact fallback (rare: a column far below the tile maximum): recompute y, exact column max
+            float y[64];
+            tmem_ld32(laddr + buf * 128, y);
+            tmem_ld32(laddr + buf * 128 + 32, y + 32);
+            tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float t[32];
+            for (int j = 0; j < 64; ++j) y[j] = (row_ok && cb + j < p.ncols) ? y[j] * k2 : -INFINITY;
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              const float4 a = *reinterpret_cast<const float4*>(&cmx[h][0][c * 32 + i]);
-              const float4 b = *reinterpret_cast<const float4*>(&cmx[h][1][c * 32 + i]);
-              const float M0 = fmaxf(a.x, b.x), M1 = fmaxf(a.y, b.y), M2 = fmaxf(a.z, b.z), M3 = fmaxf(a.w, b.w);
-              t[i + 0] = M0 == -INFINITY ? 0.f : ex2(v[c * 32 + i + 0] - M0);
-              t[i + 1] = M1 == -INFINITY ? 0.f : ex2(v[c * 32 + i + 1] - M1);
-              t[i + 2] = M2 == -INFINITY ? 0.f : ex2(v[c * 32 + i + 2] - M2);
-              t[i + 3] = M3 == -INFINITY ? 0.f : ex2(v[c * 32 + i + 3] - M3);
+            for (int i = 0; i < 32; ++i) t[i] = y[i];
+            m0 = xreduce32<true>(t, lane);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) t[i] = y[32 + i];
+            m1 = xreduce32<true>(t, lane);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float ci = __shfl_sync(0xffffffffu, m0, i);
+              t[i] = ci == -INFINITY ? 0.f : ex2(y[i] - ci);
             }
-            csum[c] = xreduce32<false>(t, lane);
-          }
+            S0 = xreduce32<false>(t, lane);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) csm[h][rh][c * 32 + lane] = csum[c];
-          named_bar_sync(2 + h, 64);
+            for (int i = 0; i < 32; ++i) {
+              const float ci = __shfl_sync(0xffffffffu, m1, i);
+              t[i] = ci == -INFINITY ? 0.f : ex2(y[32 + i] - ci);
+            }
+            S1 = xreduce32<false>(t, lane);
+          }
+          // double-buffered S: release this buffer only after the (rare) exact fallback has re-read it
+          tc_fence_before();
+          named_bar_sync(1, 256);
+          if (et == 0) mbar_arrive_cluster(&sfree[buf], 0);
+          xch[grp][rh][lane] = make_float2(m0, S0);
+          xch[grp][rh][32 + lane] = make_float2(m1, S1);
+          named_bar_sync(2 + grp, 64);
           if (rh == 0) {
-            const bool first_visit = (it - it0) < p.n_ct;
-            float2* slot = p.col_slots + (long long)blockIdx.x * p.slot_ld;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const int jl = c * 32 + lane;
-              const int jg = cbase + jl;
-              if (jg < p.ncols) {
-                float2 nw = make_float2(fmaxf(cmx[h][0][jl], cmx[h][1][jl]), csm[h][0][jl] + csm[h][1][jl]);
-                if (!first_visit) nw = merge2(slot[jg], nw);
-                slot[jg] = nw;
-              }
+            float2 a0 = merge2(xch[grp][0][lane], xch[grp][1][lane]);
+            float2 a1 = merge2(xch[grp][0][32 + lane], xch[grp][1][32 + lane]);
+            if (!first_visit) {
+              a0 = merge2(pre0, a0);
+              a1 = merge2(pre1, a1);
             }
+            if (cb + lane < p.ncols) slot[cb + lane] = a0;
+            if (cb + 32 + lane < p.ncols) slot[cb + 32 + lane] = a1;
           }
         } else {
-          // ---------------------------------------------------------- backward: G tile -> smem
-          const float* cvh = cv + h * 128;
-          uint32_t pk[64];
+          // ---------------------------------------------------------- backward: G tile -> smem (bf16)
+          const float* cv = cval[tile_ctr & 1] + h * 128 + u * 64;
+          uint32_t pk[32];
 #pragma unroll
-          for (int j = 0; j < 128; j += 4) {
-            const float4 c4 = *reinterpret_cast<const float4*>(cvh + j);
-            float g[4];
-            const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+          for (int j = 0; j < 64; j += 4) {
+            const float4 c4 = *reinterpret_cast<const float4*>(cv + j);
+            const float g0 = ex2(fmaf(v[j + 0], k2, -r2)) + ex2(fmaf(v[j + 0], k2, -c4.x));
+            const float g1 = ex2(fmaf(v[j + 1], k2, -r2)) + ex2(fmaf(v[j + 1], k2, -c4.y));
+            const float g2 = ex2(fmaf(v[j + 2], k2, -r2)) + ex2(fmaf(v[j + 2], k2, -c4.z));
+            const float g3 = ex2(fmaf(v[j + 3], k2, -r2)) + ex2(fmaf(v[j + 3], k2, -c4.w));
+            pk[j / 2] = pack_bf16(g0, g1);
+            pk[j / 2 + 1] = pack_bf16(g2, g3);
+          }
+          if (!clean) {  // ragged columns, invalid row, or the diagonal (added exactly in fp32 later)
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int jg = cbase + j + u;
-              const float y = v[j + u] * k2;
-              const bool ok = row_ok && jg < p.ncols && !(p.diag_on && jg == ig);
-              g[u] = ok ? ex2(y - r2) + ex2(y - cc[u]) : 0.f;
+            for (int j = 0; j < 64; j += 2) {
+              const int jg = cb + j;
+              const bool ok0 = row_ok && jg < p.ncols && !(p.diag_on && jg == ig);
+              const bool ok1 = row_ok && jg + 1 < p.ncols && !(p.diag_on && jg + 1 == ig);
+              pk[j / 2] &= (ok0 ? 0x0000FFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
             }
-            pk[j / 2] = pack_bf16(g[0], g[1]);
-            pk[j / 2 + 1] = pack_bf16(g[2], g[3]);
           }
           mbar_wait(&gfree, gfph ^ 1, 9);
           gfph ^= 1;
-          const uint32_t gb = smem_u32(sG) + (2 * h) * kBox + r * 128;
+          const uint32_t gb = smem_u32(sG) + (2 * h + u) * kBox + r * 128;
 #pragma unroll
-          for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-            for (int c16 = 0; c16 < 8; ++c16)
-              st_shared_v4(gb + kb * kBox + ((c16 ^ (r & 7)) << 4), pk[kb * 32 + c16 * 4 + 0], pk[kb * 32 + c16 * 4 + 1],
-                           pk[kb * 32 + c16 * 4 + 2], pk[kb * 32 + c16 * 4 + 3]);
+          for (int c16 = 0; c16 < 8; ++c16)
+            st_shared_v4(gb + ((c16 ^ (r & 7)) << 4), pk[c16 * 4 + 0], pk[c16 * 4 + 1], pk[c16 * 4 + 2],
+                         pk[c16 * 4 + 3]);
+          if (it + 1 < it1) cval[(tile_ctr + 1) & 1][et] = pre_c;
           fence_proxy_async_smem();
-          named_bar_sync(1, 128);
+          named_bar_sync(1, 256);
           if (et == 0) mbar_arrive_cluster(&gready, 0);
         }
         ++tile_ctr;
       }
       if constexpr (!BWD) {
-        // merge the two column halves of each row, write this segment's row partial
-        if (h == 1) rowx[r] = make_float2(m, sig);
-        named_bar_sync(1, 128);
-        if (h == 0 && row_ok)
-          p.row_parts[(long long)(pair + rb) * kRowsPerPair + cta * 64 + r] = merge2(make_float2(m, sig), rowx[r]);
+        // merge the 4 column slices of each row, write this segment's row partial
+        rowx[grp][r] = make_float2(m, sig);
+        named_bar_sync(1, 256);
+        if (grp == 0 && row_ok) {
+          float2 a = merge2(merge2(rowx[0][r], rowx[1][r]), merge2(rowx[2][r], rowx[3][r]));
+          p.row_parts[(long long)(pair + rb) * kRowsPerPair + cta * 64 + r] = a;
+        }
+        named_bar_sync(1, 256);
       } else {
-        // drain dA^T (128 d-rows of each 256-chunk x 128 pair rows) with red.add into dA
+        // drain dA^T: lanes = 128 d-rows of each 256-chunk, columns u*64.. = pair rows -> red.add into dA
         mbar_wait(&dafull, daph, 10);
         daph ^= 1;
         tc_fence_after();
+        const int row0 = rb * kRowsPerPair + u * 64;
         for (int tc = 0; tc < p.NDC; ++tc) {
           const int d = tc * 256 + (int)cta * 128 + q * 32 + lane;
-          const int row0 = rb * kRowsPerPair;
-          for (int c = 0; c < 4; ++c) {
-            float v[32];
-            tmem_ld32(laddr + 128 + tc * 128 + c * 32, v);
+          for (int c = 0; c < 2; ++c) {
+            float y[32];
+            tmem_ld32(laddr + 128 + tc * 128 + c * 32, y);
             tmem_ld_wait();
             if (d < p.d_out) {
 #pragma unroll
               for (int i = 0; i < 32; ++i)
                 if (row0 + c * 32 + i < p.nrows)
-                  red_add_f32(p.dA + (long long)(row0 + c * 32 + i) * p.ld_dA + d, coef * v[i]);
+                  red_add_f32(p.dA + (long long)(row0 + c * 32 + i) * p.ld_dA + d, coef * y[i]);
             }
           }
         }
         tc_fence_before();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 256);
         if (et == 0) mbar_arrive_cluster(&dafree, 0);
       }
     }

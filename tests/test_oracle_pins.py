@@ -325,3 +325,20 @@ def test_mutations_are_caught():
     fdI, fdT = brute.fd_grads(I[:5, :3].tolist(), T[:5, :3].tolist(), 2.0)
     assert not np.allclose(2 * dI, np.array(fdI), rtol=1e-3)  # losing the 1/2 of Q4 would fail
     assert not np.allclose(dT, np.array(fdI), rtol=1e-3)
+
+
+def test_backward_abs_bounds_gradient():
+    # |sum_j G_ij T_j| <= sum_j |G_ij| |T_j| (triangle inequality), with equality for nonnegative summands
+    b, d = 30, 6
+    I = rand_feats(b, d, 101)
+    T = rand_feats(b, d, 102)
+    dI, dT = O.backward(I, T, 5.0)
+    aI, aT = O.backward_abs(I, T, 5.0)
+    assert np.all(aI >= np.abs(dI) - 1e-15) and np.all(aT >= np.abs(dT) - 1e-15)
+    Ip, Tp = np.abs(I), np.abs(T)
+    cf = O.onehot_closed_form(8, 8, 8, 1.0)
+    E = np.eye(8)
+    aI1, _ = O.backward_abs(E, E, 1.0)
+    # one-hot: off-class components of dI are s*g/b*m*q >= 0 and equal their magnitude bound
+    off = ~np.eye(8, dtype=bool)
+    assert np.allclose(aI1[off], np.abs(cf["dI"][off]), atol=1e-15)
