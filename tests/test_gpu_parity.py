@@ -165,3 +165,19 @@ def test_errors():
     I, T = make_features(64, 32, seed=1)
     with pytest.raises(InfclError):
         K.infcl_forward(I.cuda(), T.cuda(), 64, float("nan"))
+
+
+def test_forward_exact_fallback_adversarial_columns():
+    """Columns far below every tile maximum (x_ij ~ -s for all i) make the shared-exponential column partial
+    underflow; the kernel must take its exact fallback."""
+    b, d = 1024, 128
+    I, T = make_features(b, d, seed=12, dist="paired")
+    I = I.float()
+    T = T.float()
+    u = torch.nn.functional.normalize(I.mean(0, keepdim=True), dim=1)
+    I = torch.nn.functional.normalize(I + 3.0 * u, dim=1)  # all images share a common direction
+    T[7] = -u[0]
+    T[300] = -u[0]
+    I = I.to(torch.bfloat16)
+    T = T.to(torch.bfloat16)
+    check_all(I, T, 100.0)
