@@ -145,6 +145,11 @@ infcl_status infcl_profile_read(int kind, int* launches, double* total_ms);
 infcl_status infcl_probe_umma(const void* A, const void* B, int M, int N, int K, int a_mn_major, int ncta,
                               float* out, int ncols, void* stream);
 
+/* MMA issue-rate probe: one CTA (pair) issues `iters` back-to-back tcgen05.mma (bf16, K=16) of shape M x N
+ * from resident smem; out_cycles (device, 2 x int64) = {issue cycles, issue-to-completion cycles}. */
+infcl_status infcl_probe_mma_rate(int M, int N, int a_mn_major, int ncta, int iters, long long* out_cycles,
+                                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,7 @@ SIGNATURES = {
     "infcl_reset_launch_count": (None, []),
     "infcl_profile_enable": (None, [_i]),
     "infcl_profile_read": (_i, [_i, ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_double)]),
+    "infcl_probe_mma_rate": (_i, [_i, _i, _i, _i, _i, _p, _p]),
     "infcl_probe_umma": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _i, _p]),
 }
 

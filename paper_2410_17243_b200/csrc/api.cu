@@ -151,7 +151,7 @@ Layout make_layout(int64_t b, int d, int world, infcl_dtype dt) {
     return at;
   };
   L.off_slots = take((size_t)2 * L.g.npairs * L.slot_ld * sizeof(float2));
-  L.off_rparts = take((size_t)(L.g.n_rb + L.g.npairs) * kRowsPerPair * sizeof(float2));
+  L.off_rparts = take((size_t)(L.g.n_rb + 2 * L.g.npairs) * kRowsPerPair * sizeof(float2));
   L.off_rstate = take((size_t)L.bs * sizeof(float2));
   L.off_cstate = take((size_t)3 * L.bs * sizeof(float2));
   L.off_own2 = take((size_t)2 * L.bs * sizeof(float));

@@ -23,15 +23,15 @@ __device__ __forceinline__ float2 merge_ms(float2 a, float2 b) {
   return make_float2(M, a.y * exp2f(a.x - M) + b.y * exp2f(b.x - M));
 }
 
-__device__ __forceinline__ long long item_begin_h(long long n_items, int npairs, int p) {
-  return (long long)p * n_items / npairs;
-}
+// Mirror of the pair kernel's schedule (pair_kernel.cu, struct Sched): full waves W = n_rb / P, then the tail
+// row blocks split into P contiguous ranges of T = R * n_ct items.
+__device__ __forceinline__ long long tail_begin(long long T, int P, int p) { return (long long)p * T / P; }
 
-__device__ int pair_of(long long item, long long n_items, int npairs) {
-  int p = (int)(((item + 1) * npairs + n_items - 1) / n_items) - 1;
-  p = max(0, min(npairs - 1, p));
-  while (p > 0 && item_begin_h(n_items, npairs, p) > item) --p;
-  while (p + 1 < npairs && item_begin_h(n_items, npairs, p + 1) <= item) ++p;
+__device__ int tail_pair_of(long long t, long long T, int P) {
+  int p = (int)(((t + 1) * P + T - 1) / T) - 1;
+  p = max(0, min(P - 1, p));
+  while (p > 0 && tail_begin(T, P, p) > t) --p;
+  while (p + 1 < P && tail_begin(T, P, p + 1) <= t) ++p;
   return p;
 }
 
@@ -40,30 +40,40 @@ __global__ void init_state_kernel(float2* st, int n) {
   if (i < n) st[i] = make_float2(-INFINITY, 0.f);
 }
 
-__global__ void merge_rows_kernel(const float2* __restrict__ parts, float2* __restrict__ state, int nrows, int n_ct,
-                                  long long n_items, int npairs) {
+__global__ void merge_rows_kernel(const float2* __restrict__ parts, float2* __restrict__ state, int nrows, int n_rb,
+                                  int n_ct, int P) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
   const int rb = i / kRowsPerPair;
-  const int p0 = pair_of((long long)rb * n_ct, n_items, npairs);
-  const int p1 = pair_of((long long)(rb + 1) * n_ct - 1, n_items, npairs);
+  const int W = n_rb / P;
   float2 acc = state[i];
-  for (int p = p0; p <= p1; ++p) acc = merge_ms(acc, parts[(long long)(p + rb) * kRowsPerPair + (i % kRowsPerPair)]);
+  if (rb < W * P) {
+    acc = merge_ms(acc, parts[(long long)rb * kRowsPerPair + (i % kRowsPerPair)]);
+  } else {
+    const long long T = (long long)(n_rb - W * P) * n_ct;
+    const long long t0 = (long long)(rb - W * P) * n_ct;
+    const int p0 = tail_pair_of(t0, T, P), p1 = tail_pair_of(t0 + n_ct - 1, T, P);
+    for (int p = p0; p <= p1; ++p)
+      acc = merge_ms(acc, parts[((long long)n_rb + p + (rb - W * P)) * kRowsPerPair + (i % kRowsPerPair)]);
+  }
   state[i] = acc;
 }
 
 __global__ void merge_cols_kernel(const float2* __restrict__ slots, long long slot_ld, float2* __restrict__ state,
-                                  int ncols, int n_ct, long long n_items, int npairs) {
+                                  int ncols, int n_rb, int n_ct, int P) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= ncols) return;
   const int ct = j / kColsPerTile;
+  const int W = n_rb / P;
+  const long long T = (long long)(n_rb - W * P) * n_ct;
   float2 acc = state[j];
-  for (int p = 0; p < npairs; ++p) {
-    const long long a = item_begin_h(n_items, npairs, p), e = item_begin_h(n_items, npairs, p + 1);
-    bool visited;
-    if (e - a >= n_ct) visited = true;
-    else if (e == a) visited = false;
-    else visited = a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e;
+  for (int p = 0; p < P; ++p) {
+    bool visited = W > 0;
+    if (!visited) {
+      const long long a = tail_begin(T, P, p), e = tail_begin(T, P, p + 1);
+      if (e - a >= n_ct) visited = true;
+      else if (e > a) visited = a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e;
+    }
     if (!visited) continue;
     acc = merge_ms(acc, slots[(long long)(2 * p) * slot_ld + j]);
     acc = merge_ms(acc, slots[(long long)(2 * p + 1) * slot_ld + j]);
@@ -153,12 +163,12 @@ void launch_init_state(float2* st, int n, cudaStream_t s) {
   ++launch_counter();
 }
 void launch_merge_rows(const float2* parts, float2* state, int nrows, const PassGeom& g, cudaStream_t s) {
-  merge_rows_kernel<<<nblk(nrows, 256), 256, 0, s>>>(parts, state, nrows, g.n_ct, g.n_items, g.npairs);
+  merge_rows_kernel<<<nblk(nrows, 256), 256, 0, s>>>(parts, state, nrows, g.n_rb, g.n_ct, g.npairs);
   ++launch_counter();
 }
 void launch_merge_cols(const float2* slots, long long slot_ld, float2* state, int ncols, const PassGeom& g,
                        cudaStream_t s) {
-  merge_cols_kernel<<<nblk(ncols, 256), 256, 0, s>>>(slots, slot_ld, state, ncols, g.n_ct, g.n_items, g.npairs);
+  merge_cols_kernel<<<nblk(ncols, 256), 256, 0, s>>>(slots, slot_ld, state, ncols, g.n_rb, g.n_ct, g.npairs);
   ++launch_counter();
 }
 void launch_finalize_lse(const float2* st, float* lse, float* lse2, int n, cudaStream_t s) {

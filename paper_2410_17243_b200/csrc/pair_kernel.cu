@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 #include <utility>
 #include <vector>
 
@@ -47,13 +49,14 @@ static void prof_clear() {
 }
 
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
-constexpr int kBox = 8192;     // one TMA box: 64 rows x 64 bf16 (128 B, SW128)
-constexpr int kStage = 16384;  // one ring stage: two boxes
+constexpr int kBox = 8192;     // A_R / G block: 64 rows x 64 bf16 (128 B, SW128)
+constexpr int kBoxB = 16384;   // streamed B box: 128 rows x 64 bf16 (128 B, SW128)
+constexpr int kStage = 32768;  // one ring stage: two B boxes (8 MMAs per barrier round trip)
 constexpr int kMaxStages = 12;
 constexpr int kSmemBudget = 232448 - 8192;  // 227 KB opt-in minus static smem and slack
 
 struct KParams {
-  int nrows, ncols, dk, KB, NDC;
+  int nrows, ncols, dk, KB, KC, NDC;
   int n_rb, n_ct, npairs, n_stages;
   long long n_items;
   float k2, scale;
@@ -68,11 +71,44 @@ struct KParams {
   int ld_dA, d_out;
   const float* grad;
   float coef_base;
+  unsigned long long* dbg;  // optional per-tag wait-cycle accumulators (INFCL_DEBUG_WAITS)
+  int noepi;                // diagnostic: epilogue skips its math (results invalid; INFCL_DEBUG_NOEPI)
 };
 
-__device__ __forceinline__ long long item_begin(long long n_items, int npairs, int p) {
-  return (long long)p * n_items / npairs;
-}
+// Column-synchronous schedule.  Full waves: pair p owns row block w*P + p for w < W = n_rb / P and sweeps all
+// column tiles in order, so all pairs stream the same B tiles at about the same time (each tile is read from
+// HBM once and served from L2 to the other pairs).  Tail: the remaining R = n_rb - W*P row blocks x n_ct tiles
+// are split into P contiguous ranges (row-major), so the last wave stays balanced.  Segment = consecutive
+// items of one row block; row-partial slot of a segment: rb (full waves) or n_rb + p + (rb - W*P) (tail).
+struct Sched {
+  int P, W, n_ct, n_rb, pair;
+  long long tb, te;  // this pair's tail range (tail item indices)
+  __device__ Sched(int n_rb_, int n_ct_, int P_, int pair_) : P(P_), n_ct(n_ct_), n_rb(n_rb_), pair(pair_) {
+    W = n_rb / P;
+    const long long T = (long long)(n_rb - W * P) * n_ct;
+    tb = (long long)pair * T / P;
+    te = (long long)(pair + 1) * T / P;
+  }
+  __device__ long long n_local() const { return (long long)W * n_ct + (te - tb); }
+  __device__ void decode(long long k, int& rb, int& ct) const {
+    const long long kw = (long long)W * n_ct;
+    if (k < kw) {
+      rb = (int)(k / n_ct) * P + pair;
+      ct = (int)(k % n_ct);
+    } else {
+      const long long t = tb + (k - kw);
+      rb = W * P + (int)(t / n_ct);
+      ct = (int)(t % n_ct);
+    }
+  }
+  __device__ long long seg_end(long long k) const {  // exclusive local index where k's segment ends
+    const long long kw = (long long)W * n_ct;
+    if (k < kw) return (k / n_ct + 1) * n_ct;
+    const long long t = tb + (k - kw);
+    return kw + std::min<long long>(te, (t / n_ct + 1) * n_ct) - tb;
+  }
+  __device__ long long seg_slot(int rb) const { return rb < W * P ? rb : (long long)n_rb + pair + (rb - W * P); }
+};
 
 __device__ __forceinline__ float2 merge2(float2 a, float2 b) {
   const float M = fmaxf(a.x, b.x);
@@ -103,7 +139,33 @@ __device__ __forceinline__ float xreduce32(float (&t)[32], int lane) {
   return t[0];
 }
 
-template <bool BWD>
+template <bool ON>
+struct WaitClock {
+  unsigned long long* dbg;
+  unsigned long long acc[ON ? 12 : 1];
+  __device__ WaitClock(unsigned long long* d) : dbg(d) {
+#pragma unroll
+    for (int i = 0; i < (ON ? 12 : 1); ++i) acc[i] = 0;
+  }
+  __device__ __forceinline__ void wait(uint64_t* bar, uint32_t par, int tag, bool cluster = false) {
+    if (!ON || !dbg) {
+      if (cluster) mbar_wait_cluster(bar, par, tag);
+      else mbar_wait(bar, par, tag);
+      return;
+    }
+    const unsigned long long t0 = clock64();
+    if (cluster) mbar_wait_cluster(bar, par, tag);
+    else mbar_wait(bar, par, tag);
+    acc[tag] += clock64() - t0;
+  }
+  __device__ void flush(int role) {
+    if (!ON || !dbg) return;
+    for (int i = 0; i < 12; ++i)
+      if (acc[i]) atomicAdd(dbg + role * 16 + i, acc[i]);
+  }
+};
+
+template <bool BWD, bool DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ KParams p) {
@@ -123,8 +185,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
-  const long long it0 = item_begin(p.n_items, p.npairs, pair);
-  const long long it1 = item_begin(p.n_items, p.npairs, pair + 1);
+  const Sched S(p.n_rb, p.n_ct, p.npairs, pair);
+  const long long nk = S.n_local();
   constexpr uint32_t kTmemCols = BWD ? 512 : 256;
 
   if (threadIdx.x == 0) {
@@ -154,54 +216,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tbase = tmem_base;
 
+  const unsigned long long t_start = DBG ? clock64() : 0ull;
   if (warp == 0) {
     // ===================================================================== TMA producer (both CTAs)
     if (lane == 0) {
+      WaitClock<DBG> wc(lane == 0 ? p.dbg : nullptr);
       int stage = 0;
       uint32_t ph = 0, aph = 0;
       auto load_stage = [&](int c0a, int c1a, int c0b, int c1b) {
-        mbar_wait(&empty[stage], ph ^ 1, 1);
+        wc.wait(&empty[stage], ph ^ 1, 1);
         if (cta == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStage);
         uint8_t* dst = sStage + stage * kStage;
         tma_load_2d_pair(dst, &tmB, &full[stage], c0a, c1a);
-        tma_load_2d_pair(dst + kBox, &tmB, &full[stage], c0b, c1b);
+        tma_load_2d_pair(dst + kBoxB, &tmB, &full[stage], c0b, c1b);
         if (++stage == p.n_stages) {
           stage = 0;
           ph ^= 1;
         }
       };
+      // S stage kc: this CTA's 128 columns j, d-blocks 2kc and 2kc+1 (K-major operand, K = d)
       auto load_S = [&](int ct) {
         const int j0 = ct * kColsPerTile + (int)cta * 128;
-        for (int kb = 0; kb < p.KB; ++kb) load_stage(kb * 64, j0, kb * 64, j0 + 64);
+        for (int kc = 0; kc < p.KC; ++kc) load_stage(kc * 128, j0, kc * 128 + 64, j0);
       };
+      // dA stage (tc, jc): 128 columns j of the tile, this CTA's 128 d-rows of chunk tc (MN-major operand, K = j)
       auto load_dA = [&](int ct) {
         for (int tc = 0; tc < p.NDC; ++tc) {
           const int d0 = tc * 256 + (int)cta * 128;
-          for (int jc = 0; jc < 4; ++jc) load_stage(d0, ct * kColsPerTile + jc * 64, d0 + 64, ct * kColsPerTile + jc * 64);
+          for (int jc = 0; jc < 2; ++jc) load_stage(d0, ct * kColsPerTile + jc * 128, d0 + 64, ct * kColsPerTile + jc * 128);
         }
       };
-      long long it = it0;
-      while (it < it1) {
-        const int rb = (int)(it / p.n_ct);
-        const long long seg_end = std::min<long long>(it1, (long long)(rb + 1) * p.n_ct);
-        mbar_wait(&afree, aph ^ 1, 2);
+      long long it = 0;
+      while (it < nk) {
+        int rb, ct0;
+        S.decode(it, rb, ct0);
+        const long long seg_end = S.seg_end(it);
+        wc.wait(&afree, aph ^ 1, 2);
         aph ^= 1;
         if (cta == 0) mbar_arrive_expect_tx(&afull, 2u * p.KB * kBox);
         for (int kb = 0; kb < p.KB; ++kb)
           tma_load_2d_pair(sA + kb * kBox, &tmA, &afull, kb * 64, rb * kRowsPerPair + (int)cta * 64);
         int prev = -1;
         for (; it < seg_end; ++it) {
-          const int ct = (int)(it % p.n_ct);
+          int rb_, ct;
+          S.decode(it, rb_, ct);
           load_S(ct);
           if (BWD && prev >= 0) load_dA(prev);
           prev = ct;
         }
         if (BWD) load_dA(prev);
       }
+      wc.flush(0);
     }
   } else if (warp == 1) {
     // ===================================================================== MMA issuer (leader CTA)
-    if (cta == 0 && lane == 0) {
+    // the whole warp runs converged (warp-uniform descriptors); elect.sync inside the asm issues
+    if (cta == 0) {
+      WaitClock<DBG> wc(lane == 0 ? p.dbg : nullptr);
       int stage = 0;
       uint32_t ph = 0, aph = 0, gph = 0, dph = 0;
       uint32_t sfph[2] = {0, 0};
@@ -216,59 +287,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       };
       auto issue_dA = [&](bool first) {
         if (first) {
-          mbar_wait_cluster(&dafree, dph ^ 1, 3);
+          wc.wait(&dafree, dph ^ 1, 3, true);
           dph ^= 1;
         }
-        mbar_wait_cluster(&gready, gph, 4);
+        wc.wait(&gready, gph, 4, true);
         gph ^= 1;
         tc_fence_after();
         for (int tc = 0; tc < p.NDC; ++tc) {
-          for (int jc = 0; jc < 4; ++jc) {
-            mbar_wait(&full[stage], ph, 5);
+          for (int jc = 0; jc < 2; ++jc) {
+            wc.wait(&full[stage], ph, 5);
             tc_fence_after();
             const uint32_t sa = smem_u32(sStage + stage * kStage);
-            const uint32_t sb = smem_u32(sG + jc * kBox);
+            const uint32_t sb = smem_u32(sG + jc * 2 * kBox);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint64_t ad = smem_desc_sw128(sa + k * 2048, kBox, 1024);  // MN-major B_C^T
-              const uint64_t bd = smem_desc_sw128(sb + k * 32, 16, 1024);      // K-major G
-              umma_bf16<2>(tbase + 128 + tc * 128, ad, bd, idD, (first && jc == 0 && k == 0) ? 0u : 1u);
+            for (int k = 0; k < 8; ++k) {
+              const uint64_t ad = smem_desc_sw128(sa + k * 2048, kBoxB, 1024);               // MN-major B_C^T
+              const uint64_t bd = smem_desc_sw128(sb + (k >> 2) * kBox + (k & 3) * 32, 16, 1024);  // K-major G
+              umma_bf16_warp<2>(tbase + 128 + tc * 128, ad, bd, idD, (first && jc == 0 && k == 0) ? 0u : 1u);
             }
-            umma_commit_pair_mc(&empty[stage], 0x3);
+            umma_commit_pair_mc_warp(&empty[stage], 0x3);
             advance();
           }
         }
-        umma_commit_pair_mc(&gfree, 0x3);
+        umma_commit_pair_mc_warp(&gfree, 0x3);
       };
-      long long it = it0;
-      while (it < it1) {
-        const int rb = (int)(it / p.n_ct);
-        const long long seg_end = std::min<long long>(it1, (long long)(rb + 1) * p.n_ct);
-        mbar_wait_cluster(&afull, aph, 6);
+      long long it = 0;
+      while (it < nk) {
+        const long long seg_end = S.seg_end(it);
+        wc.wait(&afull, aph, 6, true);
         aph ^= 1;
         tc_fence_after();
         bool have_prev = false, first_dA = true;
         for (; it < seg_end; ++it) {
           const int buf = BWD ? 0 : (tile_ctr & 1);
-          mbar_wait_cluster(&sfree[buf], sfph[buf] ^ 1, 7);
+          wc.wait(&sfree[buf], sfph[buf] ^ 1, 7, true);
           sfph[buf] ^= 1;
           tc_fence_after();
           const uint32_t dS = tbase + buf * 128;
-          for (int kb = 0; kb < p.KB; ++kb) {
-            mbar_wait(&full[stage], ph, 5);
+          for (int kc = 0; kc < p.KC; ++kc) {
+            wc.wait(&full[stage], ph, 5);
             tc_fence_after();
-            const uint32_t sa = smem_u32(sA + kb * kBox);
+            const uint32_t sa = smem_u32(sA + 2 * kc * kBox);
             const uint32_t sb = smem_u32(sStage + stage * kStage);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              umma_bf16<2>(dS, smem_desc_sw128(sa + k * 32, 16, 1024), smem_desc_sw128(sb + k * 32, 16, 1024), idS,
-                           (kb | k) != 0);
+            const int nk = (2 * kc + 1 < p.KB) ? 8 : 4;  // odd number of 64-d blocks: last stage is half used
+            for (int k = 0; k < nk; ++k) {
+              umma_bf16_warp<2>(dS, smem_desc_sw128(sa + (k >> 2) * kBox + (k & 3) * 32, 16, 1024),
+                           smem_desc_sw128(sb + (k >> 2) * kBoxB + (k & 3) * 32, 16, 1024), idS, (kc | k) != 0);
             }
-            umma_commit_pair_mc(&empty[stage], 0x3);
+            umma_commit_pair_mc_warp(&empty[stage], 0x3);
             advance();
           }
-          umma_commit_pair_mc(&sfull[buf], 0x3);
-          if (it + 1 == seg_end) umma_commit_pair_mc(&afree, 0x3);
+          umma_commit_pair_mc_warp(&sfull[buf], 0x3);
+          if (it + 1 == seg_end) umma_commit_pair_mc_warp(&afree, 0x3);
           ++tile_ctr;
           if (BWD) {
             if (have_prev) {
@@ -280,9 +350,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (BWD) {
           issue_dA(first_dA);
-          umma_commit_pair_mc(&dafull, 0x3);
+          umma_commit_pair_mc_warp(&dafull, 0x3);
         }
       }
+      wc.flush(1);
     }
   } else {
     // ===================================================================== epilogue (both CTAs)
@@ -298,44 +369,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int et = ep * 32 + lane;  // 0..255
     const uint32_t laddr = tbase + ((uint32_t)(q * 32) << 16) + u * 64;
     uint32_t sph[2] = {0, 0}, gfph = 0, daph = 0;
+    WaitClock<DBG> wc(lane == 0 ? p.dbg : nullptr);
     int tile_ctr = 0;
     const float k2 = p.k2;
     float coef = 0.f;
     if (BWD) {
       coef = p.coef_base * __ldg(p.grad);
-      if (it0 < it1) {  // column LSEs of the first tile (later tiles are prefetched one tile ahead)
-        const int j = (int)(it0 % p.n_ct) * kColsPerTile + et;
-        cval[0][et] = j < p.ncols ? __ldg(p.lse_col2 + j) : 0.f;
-      }
     }
-    long long it = it0;
-    while (it < it1) {
-      const int rb = (int)(it / p.n_ct);
-      const long long seg_end = std::min<long long>(it1, (long long)(rb + 1) * p.n_ct);
+    long long it = 0;
+    while (it < nk) {
+      int rb, ct_first;
+      S.decode(it, rb, ct_first);
+      const long long seg_end = S.seg_end(it);
+      if (BWD) {  // column LSEs of the segment's first tile (later tiles are prefetched one tile ahead)
+        const int j = ct_first * kColsPerTile + et;
+        cval[tile_ctr & 1][et] = j < p.ncols ? __ldg(p.lse_col2 + j) : 0.f;
+      }
       const int ig = rb * kRowsPerPair + (int)cta * 64 + r;
       const bool row_ok = ig < p.nrows;
       float m = -INFINITY, sig = 0.f;  // forward: running row state over this thread's column slice
       float r2 = 0.f;
       if (BWD && row_ok) r2 = __ldg(p.lse_row2 + ig);
       for (; it < seg_end; ++it) {
-        const int ct = (int)(it % p.n_ct);
+        int rb_, ct;
+        S.decode(it, rb_, ct);
         const int buf = BWD ? 0 : (tile_ctr & 1);
         const int cb = ct * kColsPerTile + h * 128 + u * 64;  // global column of this thread's column 0
         const bool diag_tile = p.diag_on && ig >= cb && ig < cb + 64;
         const bool clean = row_ok && (cb + 64 <= p.ncols) && !diag_tile;
         float pre_c = 0.f;  // backward: next tile's column LSE (prefetch)
-        if (BWD && it + 1 < it1) {
-          const int j = (int)((it + 1) % p.n_ct) * kColsPerTile + et;
+        if (BWD && it + 1 < seg_end) {
+          int rbn, ctn;
+          S.decode(it + 1, rbn, ctn);
+          const int j = ctn * kColsPerTile + et;
           pre_c = j < p.ncols ? __ldg(p.lse_col2 + j) : 0.f;
         }
         float2 pre0 = make_float2(-INFINITY, 0.f), pre1 = pre0;  // forward: slot values (prefetch)
-        const bool first_visit = (it - it0) < p.n_ct;
+        const bool first_visit = it < p.n_ct;
         float2* slot = p.col_slots + (long long)blockIdx.x * p.slot_ld;
         if (!BWD && rh == 0 && !first_visit) {
           if (cb + lane < p.ncols) pre0 = slot[cb + lane];
           if (cb + 32 + lane < p.ncols) pre1 = slot[cb + 32 + lane];
         }
-        mbar_wait(&sfull[buf], sph[buf], 8);
+        wc.wait(&sfull[buf], sph[buf], 8);
         sph[buf] ^= 1;
         tc_fence_after();
         float v[64];
@@ -348,7 +424,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (et == 0) mbar_arrive_cluster(&sfree[buf], 0);
         }
 
-        if constexpr (!BWD) {
+        if (DBG && p.noepi) {
+          if (!BWD) {
+            tc_fence_before();
+            named_bar_sync(1, 256);
+            if (et == 0) mbar_arrive_cluster(&sfree[buf], 0);
+          } else {
+            wc.wait(&gfree, gfph ^ 1, 9);
+            gfph ^= 1;
+            fence_proxy_async_smem();
+            named_bar_sync(1, 256);
+            if (et == 0) mbar_arrive_cluster(&gready, 0);
+          }
+        } else if constexpr (!BWD) {
           // ---------------------------------------------------------- forward statistics
           if (diag_tile && row_ok && p.diag_out) {
             float dv = 0.f;
@@ -466,14 +554,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               pk[j / 2] &= (ok0 ? 0x0000FFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
             }
           }
-          mbar_wait(&gfree, gfph ^ 1, 9);
+          wc.wait(&gfree, gfph ^ 1, 9);
           gfph ^= 1;
           const uint32_t gb = smem_u32(sG) + (2 * h + u) * kBox + r * 128;
 #pragma unroll
           for (int c16 = 0; c16 < 8; ++c16)
             st_shared_v4(gb + ((c16 ^ (r & 7)) << 4), pk[c16 * 4 + 0], pk[c16 * 4 + 1], pk[c16 * 4 + 2],
                          pk[c16 * 4 + 3]);
-          if (it + 1 < it1) cval[(tile_ctr + 1) & 1][et] = pre_c;
+          if (it + 1 < seg_end) cval[(tile_ctr + 1) & 1][et] = pre_c;
           fence_proxy_async_smem();
           named_bar_sync(1, 256);
           if (et == 0) mbar_arrive_cluster(&gready, 0);
@@ -486,12 +574,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         named_bar_sync(1, 256);
         if (grp == 0 && row_ok) {
           float2 a = merge2(merge2(rowx[0][r], rowx[1][r]), merge2(rowx[2][r], rowx[3][r]));
-          p.row_parts[(long long)(pair + rb) * kRowsPerPair + cta * 64 + r] = a;
+          p.row_parts[S.seg_slot(rb) * kRowsPerPair + cta * 64 + r] = a;
         }
         named_bar_sync(1, 256);
       } else {
         // drain dA^T: lanes = 128 d-rows of each 256-chunk, columns u*64.. = pair rows -> red.add into dA
-        mbar_wait(&dafull, daph, 10);
+        wc.wait(&dafull, daph, 10);
         daph ^= 1;
         tc_fence_after();
         const int row0 = rb * kRowsPerPair + u * 64;
@@ -514,8 +602,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (et == 0) mbar_arrive_cluster(&dafree, 0);
       }
     }
+    wc.flush(2 + (ep & 1));
   }
   __syncwarp();
+  if (DBG && p.dbg && threadIdx.x == 0) atomicAdd(p.dbg + 4 * 16 + 15, (unsigned long long)(clock64() - t_start));
   tc_fence_before();
   cluster_sync();
   if (warp == 1) tmem_dealloc<2>(tbase, kTmemCols);
@@ -528,6 +618,7 @@ PassGeom pass_geom(int nrows, int ncols) {
   g.n_ct = (ncols + kColsPerTile - 1) / kColsPerTile;
   g.n_items = (long long)g.n_rb * g.n_ct;
   int pairs = std::max(1, num_sms() / 2);
+  if (const char* e = getenv("INFCL_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(e)));  // diagnostic
   g.npairs = (int)std::min<long long>(pairs, g.n_items);
   return g;
 }
@@ -541,6 +632,7 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.ncols = a.ncols;
   k.dk = a.dk;
   k.KB = (a.dk + 63) / 64;
+  k.KC = (k.KB + 1) / 2;
   k.NDC = (a.dk + 255) / 256;
   k.n_rb = g.n_rb;
   k.n_ct = g.n_ct;
@@ -560,9 +652,17 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.d_out = a.d_out;
   k.grad = a.grad;
   k.coef_base = a.coef_base;
+  static unsigned long long* dbg_buf = nullptr;
+  static const bool dbg_on = getenv("INFCL_DEBUG_WAITS") != nullptr;
+  if (dbg_on) {
+    if (!dbg_buf) cudaMalloc(&dbg_buf, 5 * 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(dbg_buf, 0, 5 * 16 * sizeof(unsigned long long), s);
+    k.dbg = dbg_buf;
+  }
   const size_t fixed = 1024 + (size_t)k.KB * kBox + (BWD ? 4 * kBox : 0);
   int ns = (int)((kSmemBudget - (long long)fixed) / kStage);
   ns = std::min(ns, kMaxStages);
+  if (const char* e = getenv("INFCL_STAGES")) ns = std::max(2, std::min(ns, atoi(e)));
   if (ns < 2) return fail(INFCL_ERR_SHAPE, "feature dim too large for the smem budget");
   k.n_stages = ns;
   const size_t smem = fixed + (size_t)ns * kStage;
@@ -570,9 +670,10 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   CUtensorMap tmA, tmB;
   infcl_status st = make_tmap_bf16(&tmA, a.A, a.nrows, a.dk, a.ld, 64, 64);
   if (st) return st;
-  if ((st = make_tmap_bf16(&tmB, a.B, a.ncols, a.dk, a.ld, 64, 64))) return st;
+  if ((st = make_tmap_bf16(&tmB, a.B, a.ncols, a.dk, a.ld, 64, 128))) return st;
 
-  auto kern = pair_kernel<BWD>;
+  k.noepi = getenv("INFCL_DEBUG_NOEPI") != nullptr;
+  auto kern = dbg_on ? pair_kernel<BWD, true> : pair_kernel<BWD, false>;
   INFCL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (prof().on) {
@@ -585,6 +686,20 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   if (prof().on) {
     cudaEventRecord(e1, s);
     prof().ev[BWD ? 1 : 0].push_back({e0, e1});
+  }
+  if (dbg_on) {  // debug only: per-role mean wait cycles per CTA (roles: 0 TMA, 1 MMA, 2/3 epilogue lanes)
+    unsigned long long h[80];
+    cudaMemcpyAsync(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const double nctas = 2.0 * g.npairs;
+    fprintf(stderr, "[infcl dbg] %s kernel: mean cycles/CTA total=%.0f\n", BWD ? "BWD" : "FWD", h[4 * 16 + 15] / nctas);
+    const char* names[12] = {"-", "empty", "afree", "dafree", "gready", "full", "afull", "sfree", "sfull", "gfree",
+                             "dafull", "-"};
+    for (int role = 0; role < 4; ++role)
+      for (int t = 0; t < 12; ++t)
+        if (h[role * 16 + t])
+          fprintf(stderr, "[infcl dbg]   role %d wait %-7s %12.0f\n", role, names[t],
+                  h[role * 16 + t] / (role >= 2 ? nctas * 4 : (role == 1 ? nctas / 2 : nctas)));
   }
   ++launch_counter();
   return INFCL_OK;

@@ -117,3 +117,205 @@ extern "C" infcl_status infcl_probe_umma(const void* A, const void* B, int M, in
   }
   return INFCL_OK;
 }
+
+// ------------------------------------------------------------------ MMA issue-rate microbenchmark
+// Operands resident in smem (contents irrelevant), one thread of the leader CTA issues `iters` back-to-back
+// MMAs of the given shape, then commits; cycles per MMA are measured on the issuing SM.
+namespace infcl {
+template <int NCTA>
+__global__ void __launch_bounds__(128, 1) probe_rate_kernel(int M, int N, int a_mn, int iters, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar_done, bar_ready, bar_dummy;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x / 32;
+  const uint32_t cta = NCTA == 2 ? cluster_ctarank() : 0;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3f803f80u;
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_done, 1);
+    mbar_init(&bar_ready, 1);
+    mbar_init(&bar_dummy, 1 << 19);
+    fence_mbar_init();
+    mbar_arrive(&bar_ready);  // phase 0 completes: waits on it return at once
+  }
+  if (warp == 1) tmem_alloc<NCTA>(&tmem_base, 512);
+  tc_fence_before();
+  if constexpr (NCTA == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  if (cta == 0 && threadIdx.x == 32) {
+    const uint32_t idesc = idesc_bf16(M, N, a_mn & 1, 0);
+    const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);
+    const long long t0 = clock64();
+    // a_mn >= 2 encodes a grouped loop: every G = a_mn >> 1 MMAs do a try_wait on a completed barrier, a
+    // tcgen05 fence and a commit (the pair kernel's per-stage overhead)
+    const int G = a_mn >= 2 ? (a_mn >> 1) : 0;
+    const int amn = a_mn & 1;
+    for (int i = 0; i < iters; ++i) {
+      const int k = i & 3;
+      if (G && (i % G) == 0) {
+        mbar_wait(&bar_ready, 0);
+        tc_fence_after();
+      }
+      uint64_t ad = amn ? smem_desc_sw128(sa + k * 2048, 8192, 1024) : smem_desc_sw128(sa + k * 32, 16, 1024);
+      uint64_t bd = smem_desc_sw128(sb + k * 32, 16, 1024);
+      umma_bf16<NCTA>(tbase, ad, bd, idesc, 1);
+      if (G && (i % G) == G - 1) {
+        if constexpr (NCTA == 2) umma_commit_pair_mc(&bar_dummy, 0x3);
+        else umma_commit_1cta(&bar_dummy);
+      }
+    }
+    const long long t1 = clock64();
+    if constexpr (NCTA == 2) umma_commit_pair_mc(&bar_done, 0x3);
+    else umma_commit_1cta(&bar_done);
+    mbar_wait(&bar_done, 0);
+    const long long t2 = clock64();
+    out[0] = t1 - t0;
+    out[1] = t2 - t0;
+  }
+  if (cta != 0 || threadIdx.x != 32) mbar_wait(&bar_done, 0);
+  tc_fence_before();
+  if constexpr (NCTA == 2) cluster_sync(); else __syncthreads();
+  if (warp == 1) tmem_dealloc<NCTA>(tbase, 512);
+}
+}  // namespace infcl
+
+extern "C" infcl_status infcl_probe_mma_rate(int M, int N, int a_mn_major, int ncta, int iters, long long* out_cycles,
+                                             void* stream) {
+  if (!out_cycles || (ncta != 1 && ncta != 2) || iters < 1) return fail(INFCL_ERR_INVALID_ARG, "bad probe args");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncta);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = 64 * 1024 + 1024;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ncta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (ncta == 1) {
+    INFCL_CUDA_TRY(cudaFuncSetAttribute(probe_rate_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65 * 1024));
+    INFCL_CUDA_TRY(cudaLaunchKernelEx(&cfg, probe_rate_kernel<1>, M, N, a_mn_major, iters, out_cycles));
+  } else {
+    INFCL_CUDA_TRY(cudaFuncSetAttribute(probe_rate_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65 * 1024));
+    INFCL_CUDA_TRY(cudaLaunchKernelEx(&cfg, probe_rate_kernel<2>, M, N, a_mn_major, iters, out_cycles));
+  }
+  return INFCL_OK;
+}
+
+// co-resident cluster count for a 1-CTA-per-SM kernel (diagnostic; not part of the ABI)
+extern "C" int infcl_diag_max_clusters(int cluster) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster * 64);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = 200 * 1024;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaFuncSetAttribute(probe_rate_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (cluster > 8) cudaFuncSetAttribute(probe_rate_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  int n = -1;
+  cudaError_t e = cudaOccupancyMaxActiveClusters(&n, probe_rate_kernel<1>, &cfg);
+  return e == cudaSuccess ? n : -(int)e;
+}
+
+// ------------------------------------------------------------------ TMA streaming-throughput microbenchmark
+// Every CTA streams `iters` 16-KB (or 32-KB) stages through a ring of 6 smem stages; a consumer thread releases
+// each stage as soon as it lands.  mode 0: two 2D boxes [64 x 64 rows]; 1: one 2D box [64 x 128 rows];
+// 2: one 3D box (64, 64 rows, 2 column blocks); 3: one 2D box [64 x 256 rows] (32-KB stage).
+namespace infcl {
+__global__ void __launch_bounds__(64, 1)
+    probe_tma_kernel(const __grid_constant__ CUtensorMap t2a, const __grid_constant__ CUtensorMap t2b,
+                     const __grid_constant__ CUtensorMap t3, int mode, int iters, int nrows, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int NS = 6;
+  __shared__ uint64_t full[NS], empty[NS];
+  const int stage_bytes = mode == 3 ? 32768 : 16384;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const long long t0 = clock64();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    uint32_t ph = 0;
+    int row = (blockIdx.x * 997) % (nrows - 256);
+    for (int i = 0; i < iters; ++i) {
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_arrive_expect_tx(&full[s], stage_bytes);
+      uint8_t* dst = smem + s * 32768;
+      const int col = (i & 7) * 64;
+      if (mode == 0) {
+        tma_load_2d(dst, &t2a, &full[s], col, row);
+        tma_load_2d(dst + 8192, &t2a, &full[s], col, row + 64);
+      } else if (mode == 1) {
+        tma_load_2d(dst, &t2b, &full[s], col, row);
+      } else if (mode == 2) {
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+            "[%2];" ::"r"(smem_u32(dst)),
+            "l"(reinterpret_cast<uint64_t>(&t3)), "r"(smem_u32(&full[s])), "r"(0), "r"(row), "r"((i & 3) * 2)
+            : "memory");
+      } else {
+        tma_load_2d(dst, &t2b, &full[s], col, row);
+        tma_load_2d(dst + 16384, &t2b, &full[s], col, row + 128);
+      }
+      row += 256;
+      if (row >= nrows - 256) row -= nrows - 512;
+      if (++s == NS) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (threadIdx.x == 32) {
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < iters; ++i) {
+      mbar_wait(&full[s], ph);
+      mbar_arrive(&empty[s]);
+      if (++s == NS) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    out[blockIdx.x] = clock64() - t0;
+  }
+}
+}  // namespace infcl
+
+extern "C" int infcl_diag_tma_rate(const void* X, int nrows, int d, int mode, int iters, int nblocks, long long* out) {
+  CUtensorMap a, b, c;
+  if (make_tmap_bf16(&a, X, nrows, d, d, 64, 64) || make_tmap_bf16(&b, X, nrows, d, d, 64, 128)) return -1;
+  // 3D view: (64 inner elements, rows, column blocks of 64) with strides (row: d*2 B, block: 128 B)
+  {
+    typedef CUresult (*Fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    cuuint64_t dims[3] = {64, (cuuint64_t)nrows, (cuuint64_t)(d / 64)};
+    cuuint64_t strides[2] = {(cuuint64_t)d * 2, 128};
+    cuuint32_t box[3] = {64, 64, 2};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (reinterpret_cast<Fn>(p)(&c, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(X), dims, strides, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -2;
+  }
+  cudaFuncSetAttribute(probe_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 32768 + 1024);
+  probe_tma_kernel<<<nblocks, 64, 6 * 32768 + 1024>>>(a, b, c, mode, iters, nrows, out);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : -3;
+}
