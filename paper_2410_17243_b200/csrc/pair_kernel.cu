@@ -53,7 +53,6 @@ constexpr int kBox = 8192;     // A_R / G block: 64 rows x 64 bf16 (128 B, SW128
 constexpr int kBoxB = 16384;   // streamed B box: 128 rows x 64 bf16 (128 B, SW128)
 constexpr int kStage = 32768;  // one ring stage: two B boxes (8 MMAs per barrier round trip)
 constexpr int kMaxStages = 12;
-constexpr int kSmemBudget = 232448 - 8192;  // 227 KB opt-in minus static smem and slack
 
 struct KParams {
   int nrows, ncols, dk, KB, KC, NDC;
@@ -169,8 +168,9 @@ template <bool BWD, bool DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ KParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];  // SW128 operands need 1024-B alignment
+  uint8_t* smem = smem_raw;
+  if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u)) __trap();  // fail loudly, never silently misalign
   uint8_t* sA = smem;
   uint8_t* sG = sA + p.KB * kBox;
   uint8_t* sStage = sG + (BWD ? 4 * kBox : 0);
@@ -297,14 +297,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int jc = 0; jc < 2; ++jc) {
             wc.wait(&full[stage], ph, 5);
             tc_fence_after();
-            const uint32_t sa = smem_u32(sStage + stage * kStage);
-            const uint32_t sb = smem_u32(sG + jc * 2 * kBox);
+            // descriptors advance by adding (byte offset >> 4) to the start-address field
+            const uint64_t ad0 = smem_desc_sw128(smem_u32(sStage + stage * kStage), kBoxB, 1024);  // MN-major B_C^T
+            const uint64_t bd0 = smem_desc_sw128(smem_u32(sG + jc * 2 * kBox), 16, 1024);           // K-major G
+            const uint32_t dD = tbase + 128 + tc * 128;
+            umma_bf16_warp<2>(dD, ad0, bd0, idD, (first && jc == 0) ? 0u : 1u);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const uint64_t ad = smem_desc_sw128(sa + k * 2048, kBoxB, 1024);               // MN-major B_C^T
-              const uint64_t bd = smem_desc_sw128(sb + (k >> 2) * kBox + (k & 3) * 32, 16, 1024);  // K-major G
-              umma_bf16_warp<2>(tbase + 128 + tc * 128, ad, bd, idD, (first && jc == 0 && k == 0) ? 0u : 1u);
-            }
+            for (int k = 1; k < 8; ++k)
+              umma_bf16_warp<2>(dD, ad0 + (uint64_t)(k * (2048 >> 4)),
+                                bd0 + (uint64_t)((k >> 2) * (kBox >> 4) + (k & 3) * 2), idD, 1u);
             umma_commit_pair_mc_warp(&empty[stage], 0x3);
             advance();
           }
@@ -327,12 +328,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int kc = 0; kc < p.KC; ++kc) {
             wc.wait(&full[stage], ph, 5);
             tc_fence_after();
-            const uint32_t sa = smem_u32(sA + 2 * kc * kBox);
-            const uint32_t sb = smem_u32(sStage + stage * kStage);
-            const int nk = (2 * kc + 1 < p.KB) ? 8 : 4;  // odd number of 64-d blocks: last stage is half used
-            for (int k = 0; k < nk; ++k) {
-              umma_bf16_warp<2>(dS, smem_desc_sw128(sa + (k >> 2) * kBox + (k & 3) * 32, 16, 1024),
-                           smem_desc_sw128(sb + (k >> 2) * kBoxB + (k & 3) * 32, 16, 1024), idS, (kc | k) != 0);
+            const uint64_t ad0 = smem_desc_sw128(smem_u32(sA + 2 * kc * kBox), 16, 1024);
+            const uint64_t bd0 = smem_desc_sw128(smem_u32(sStage + stage * kStage), 16, 1024);
+            umma_bf16_warp<2>(dS, ad0, bd0, idS, kc != 0);
+#pragma unroll
+            for (int k = 1; k < 4; ++k) umma_bf16_warp<2>(dS, ad0 + (uint64_t)(2 * k), bd0 + (uint64_t)(2 * k), idS, 1u);
+            if (2 * kc + 1 < p.KB) {  // odd number of 64-d blocks: the last stage is half used
+#pragma unroll
+              for (int k = 4; k < 8; ++k)
+                umma_bf16_warp<2>(dS, ad0 + (uint64_t)((kBox >> 4) + 2 * (k & 3)),
+                                  bd0 + (uint64_t)((kBoxB >> 4) + 2 * (k & 3)), idS, 1u);
             }
             umma_commit_pair_mc_warp(&empty[stage], 0x3);
             advance();
@@ -659,8 +664,16 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
     cudaMemsetAsync(dbg_buf, 0, 5 * 16 * sizeof(unsigned long long), s);
     k.dbg = dbg_buf;
   }
-  const size_t fixed = 1024 + (size_t)k.KB * kBox + (BWD ? 4 * kBox : 0);
-  int ns = (int)((kSmemBudget - (long long)fixed) / kStage);
+  // dynamic smem starts after the static part rounded up to 1024 B (the extern array's alignment)
+  static int static_smem = -1;
+  if (static_smem < 0) {
+    cudaFuncAttributes fa;
+    INFCL_CUDA_TRY(cudaFuncGetAttributes(&fa, pair_kernel<BWD, false>));
+    static_smem = (int)fa.sharedSizeBytes;
+  }
+  const long long budget = 232448 - ((static_smem + 1023) / 1024) * 1024;
+  const size_t fixed = (size_t)k.KB * kBox + (BWD ? 4 * kBox : 0);
+  int ns = (int)((budget - (long long)fixed) / kStage);
   ns = std::min(ns, kMaxStages);
   if (const char* e = getenv("INFCL_STAGES")) ns = std::max(2, std::min(ns, atoi(e)));
   if (ns < 2) return fail(INFCL_ERR_SHAPE, "feature dim too large for the smem budget");
