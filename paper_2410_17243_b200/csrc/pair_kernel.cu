@@ -12,8 +12,9 @@
 //              (d split across the pair: 128 d-rows per SM), N=128, K=256, B_C read MN-major from the same
 //              TMA tiles layout.  The dA accumulator stays in TMEM across the whole row block (Alg.4
 //              l.12 "dI += ..."), and is drained with red.add at the end of the row block.
-// Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM alloc + MMA issuer (leader CTA), warps 2-9
-// epilogue (TMEM lane quarter = warp % 4, column slice = (warp - 2) / 4).
+// Warp roles (320 threads): warps 0-7 epilogue (TMEM lane quarter = warp % 4, column slice = warp / 4), warp 8 TMA
+// producer, warp 9 TMEM alloc + MMA issuer (leader CTA).  The issuers get the highest warp ids because the warp
+// arbiter favours higher ids: they must not lose issue slots to the epilogue warps sharing their sub-partition.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -48,7 +49,8 @@ static void prof_clear() {
   for (auto& v : prof().ev) v.clear();
 }
 
-constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+constexpr int kThreads = 320;  // warps 0-7 epilogue, warp 8 TMA, warp 9 MMA
+constexpr int kWarpTMA = 8, kWarpMMA = 9;
 constexpr int kBox = 8192;     // A_R / G block: 64 rows x 64 bf16 (128 B, SW128)
 constexpr int kBoxB = 16384;   // streamed B box: 128 rows x 64 bf16 (128 B, SW128)
 constexpr int kStage = 32768;  // one ring stage: two B boxes (8 MMAs per barrier round trip)
@@ -206,18 +208,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mbar_init(&dafree, 2);
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == kWarpTMA && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
-  if (warp == 1) tmem_alloc<2>(&tmem_base, kTmemCols);
+  if (warp == kWarpMMA) tmem_alloc<2>(&tmem_base, kTmemCols);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tbase = tmem_base;
 
   const unsigned long long t_start = DBG ? clock64() : 0ull;
-  if (warp == 0) {
+  if (warp == kWarpTMA) {
     // ===================================================================== TMA producer (both CTAs)
     if (lane == 0) {
       WaitClock<DBG> wc(lane == 0 ? p.dbg : nullptr);
@@ -268,7 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       wc.flush(0);
     }
-  } else if (warp == 1) {
+  } else if (warp == kWarpMMA) {
     // ===================================================================== MMA issuer (leader CTA)
     // the whole warp runs converged (warp-uniform descriptors); elect.sync inside the asm issues
     if (cta == 0) {
@@ -364,7 +366,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================================================================== epilogue (both CTAs)
     // 8 warps: warp w reads TMEM lane quarter q = w % 4 (rows) and column slice u = (w - 2) / 4 of 64 columns.
     // 2x2 layout of the S tile: quarter q -> rows 32*(q&1).., tile columns h*128 + u*64 + [0,64), h = q >> 1.
-    const int ep = warp - 2;
+    const int ep = warp;
     const int q = warp & 3;
     const int u = ep >> 2;
     const int h = q >> 1;
@@ -392,7 +394,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       const int ig = rb * kRowsPerPair + (int)cta * 64 + r;
       const bool row_ok = ig < p.nrows;
-      float m = -INFINITY, sig = 0.f;  // forward: running row state over this thread's column slice
+      // forward (16x256b layout): running (m, sigma) of this thread's 4 rows over its 16-column slice
+      float mrow[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, srow[4] = {0.f, 0.f, 0.f, 0.f};
       float r2 = 0.f;
       if (BWD && row_ok) r2 = __ldg(p.lse_row2 + ig);
       for (; it < seg_end; ++it) {
@@ -413,15 +416,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const bool first_visit = it < p.n_ct;
         float2* slot = p.col_slots + (long long)blockIdx.x * p.slot_ld;
         if (!BWD && rh == 0 && !first_visit) {
-          if (cb + lane < p.ncols) pre0 = slot[cb + lane];
-          if (cb + 32 + lane < p.ncols) pre1 = slot[cb + 32 + lane];
+          if (cb + 2 * lane < p.ncols) pre0 = slot[cb + 2 * lane];
+          if (cb + 2 * lane + 1 < p.ncols) pre1 = slot[cb + 2 * lane + 1];
         }
         wc.wait(&sfull[buf], sph[buf], 8);
         sph[buf] ^= 1;
         tc_fence_after();
         float v[64];
-        tmem_ld32(laddr + buf * 128, v);
-        tmem_ld32(laddr + buf * 128 + 32, v + 32);
+        if constexpr (BWD) {  // 32x32b: thread = one row, 64 consecutive columns
+          tmem_ld32(laddr + buf * 128, v);
+          tmem_ld32(laddr + buf * 128 + 32, v + 32);
+        } else {  // 16x256b: thread = 4 rows x 16 columns (see forward statistics below)
+          tmem_ld16x256x8(laddr + buf * 128, v);
+          tmem_ld16x256x8(laddr + (16u << 16) + buf * 128, v + 32);
+        }
         tmem_ld_wait();
         if constexpr (BWD) {  // single S buffer: release it as soon as it is in registers
           tc_fence_before();
@@ -443,98 +451,189 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         } else if constexpr (!BWD) {
           // ---------------------------------------------------------- forward statistics
-          if (diag_tile && row_ok && p.diag_out) {
-            float dv = 0.f;
+          // 16x256b layout: t0 = lane & 3, t1 = lane >> 2; value v[eta*32 + rho*4 + kap*2 + c] is
+          //   row  32*rh + 16*eta + 8*kap + t1 (of this CTA's 64),  column cb + 8*rho + 2*t0 + c.
+          // Row references are thread-local maxima (any upper bound works for shared exponentials), so rows
+          // need no shuffles; column sums reduce 4 rows in-thread, then 8 lanes (3 butterfly rounds).
+          const int t0 = lane & 3, t1 = lane >> 2;
+          const int rowbase = rb * kRowsPerPair + (int)cta * 64 + rh * 32 + t1;
+          bool rok[4];
 #pragma unroll
-            for (int j = 0; j < 64; ++j) dv = (cb + j == ig) ? v[j] : dv;
-            p.diag_out[ig] = dv * p.scale;
-          }
-          float mt = -INFINITY;
+          for (int ri = 0; ri < 4; ++ri) rok[ri] = rowbase + 16 * (ri >> 1) + 8 * (ri & 1) < p.nrows;
+          if (p.diag_on && p.diag_out && rowbase < cb + 64 && rowbase + 32 > cb) {  // diagonal tile (rare)
 #pragma unroll
-          for (int j = 0; j < 64; ++j) {
-            v[j] *= k2;
-            mt = fmaxf(mt, v[j]);
-          }
-          if (!(row_ok && cb + 64 <= p.ncols)) {  // ragged tile: mask columns / invalid row
-            mt = -INFINITY;
+            for (int ri = 0; ri < 4; ++ri) {
+              const int rg = rowbase + 16 * (ri >> 1) + 8 * (ri & 1);
+              const int o = rg - cb;
+              if (rok[ri] && o >= 0 && o < 64 && ((o >> 1) & 3) == t0) {
+                float dv = 0.f;
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-              v[j] = (row_ok && cb + j < p.ncols) ? v[j] : -INFINITY;
-              mt = fmaxf(mt, v[j]);
+                for (int rho = 0; rho < 8; ++rho)
+#pragma unroll
+                  for (int c = 0; c < 2; ++c)
+                    dv = (8 * rho + 2 * t0 + c == o) ? v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + c] : dv;
+                p.diag_out[rg] = dv * p.scale;
+              }
             }
           }
-          // shared exponentials: E_j = 2^{y_j - mt} serves the row sum and (weighted) the column sums
-          float acc = 0.f;
-          if (mt != -INFINITY) {
+          const bool ragged = !(rok[0] && rok[1] && rok[2] && rok[3]) || cb + 64 > p.ncols;
+          if (ragged) {
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-              v[j] = ex2(v[j] - mt);
-              acc += v[j];
+            for (int i = 0; i < 64; ++i) {
+              const int ri = (i >> 5) * 2 + ((i >> 1) & 1);
+              const int col = cb + 8 * ((i >> 2) & 7) + 2 * t0 + (i & 1);
+              v[i] = (rok[ri] && col < p.ncols) ? v[i] : -INFINITY;
             }
-            const float mn = fmaxf(m, mt);
-            sig = sig * ex2(m - mn) + acc * ex2(mt - mn);
-            m = mn;
-          } else {
-#pragma unroll
-            for (int j = 0; j < 64; ++j) v[j] = 0.f;
           }
-          float Rw = mt;  // tile-local reference of this warp's 32 rows
+          float ml[4];  // per-row local maxima (log2 units)
+#pragma unroll
+          for (int ri = 0; ri < 4; ++ri) {
+            float mv = -INFINITY;
+#pragma unroll
+            for (int rho = 0; rho < 8; ++rho)
+#pragma unroll
+              for (int c = 0; c < 2; ++c) mv = fmaxf(mv, v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + c]);
+            ml[ri] = mv == -INFINITY ? -INFINITY : mv * k2;
+          }
+          // shared exponentials E = 2^{y - ml} (y = v * s * log2 e), row sums
+#pragma unroll
+          for (int ri = 0; ri < 4; ++ri) {
+            float acc = 0.f;
+            if (ml[ri] != -INFINITY) {
+#pragma unroll
+              for (int rho = 0; rho < 8; ++rho)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                  float& x = v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + c];
+                  x = ex2(fmaf(x, k2, -ml[ri]));
+                  acc += x;
+                }
+              const float mn = fmaxf(mrow[ri], ml[ri]);
+              srow[ri] = srow[ri] * ex2(mrow[ri] - mn) + acc * ex2(ml[ri] - mn);
+              mrow[ri] = mn;
+            } else {
+#pragma unroll
+              for (int rho = 0; rho < 8; ++rho)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + c] = 0.f;
+            }
+          }
+          float Rw = fmaxf(fmaxf(ml[0], ml[1]), fmaxf(ml[2], ml[3]));
 #pragma unroll
           for (int o = 16; o; o >>= 1) Rw = fmaxf(Rw, __shfl_xor_sync(0xffffffffu, Rw, o));
-          const float w = (mt == -INFINITY) ? 0.f : ex2(mt - Rw);
-          float t[32];
+          float w[4];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) t[i] = v[i] * w;
-          float S0 = xreduce32<false>(t, lane);
+          for (int ri = 0; ri < 4; ++ri) w[ri] = ml[ri] == -INFINITY ? 0.f : ex2(ml[ri] - Rw);
+          float P[16];  // column partials over this thread's 4 rows: index rho*2 + c
 #pragma unroll
-          for (int i = 0; i < 32; ++i) t[i] = v[32 + i] * w;
-          float S1 = xreduce32<false>(t, lane);
+          for (int rho = 0; rho < 8; ++rho)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              float a = v[rho * 4 + c] * w[0];
+              a = fmaf(v[rho * 4 + 2 + c], w[1], a);
+              a = fmaf(v[32 + rho * 4 + c], w[2], a);
+              a = fmaf(v[32 + rho * 4 + 2 + c], w[3], a);
+              P[rho * 2 + c] = a;
+            }
+          // transposed butterfly over lane bits 4,3,2 -> lane holds columns 2*lane, 2*lane+1
+#define XR16(O, N)                                                     \
+  {                                                                    \
+    const bool up = (lane & (O)) != 0;                                 \
+    _Pragma("unroll") for (int i = 0; i < (N); ++i) {                  \
+      const float send = up ? P[i] : P[i + (N)];                       \
+      const float keep = up ? P[i + (N)] : P[i];                       \
+      P[i] = keep + __shfl_xor_sync(0xffffffffu, send, (O));           \
+    }                                                                  \
+  }
+          XR16(16, 8)
+          XR16(8, 4)
+          XR16(4, 2)
+#undef XR16
+          float S0 = P[0], S1 = P[1];
           float m0 = Rw, m1 = Rw;
-          const bool bad = Rw != -INFINITY && ((cb + lane < p.ncols && S0 < 8.6736174e-19f) ||
-                                               (cb + 32 + lane < p.ncols && S1 < 8.6736174e-19f));  // < 2^-60
+          const bool bad = Rw != -INFINITY && ((cb + 2 * lane < p.ncols && S0 < 8.6736174e-19f) ||
+                                               (cb + 2 * lane + 1 < p.ncols && S1 < 8.6736174e-19f));  // < 2^-60
           if (__any_sync(0xffffffffu, bad)) {
-            // exact fallback (rare: a column far below the tile maximum): recompute y, exact column max
+            // exact fallback (rare: a column far below the tile maximum): exact column max, second exponential
             float y[64];
-            tmem_ld32(laddr + buf * 128, y);
-            tmem_ld32(laddr + buf * 128 + 32, y + 32);
+            tmem_ld16x256x8(laddr + buf * 128, y);
+            tmem_ld16x256x8(laddr + (16u << 16) + buf * 128, y + 32);
             tmem_ld_wait();
+            float cm[16];
 #pragma unroll
-            for (int j = 0; j < 64; ++j) y[j] = (row_ok && cb + j < p.ncols) ? y[j] * k2 : -INFINITY;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) t[i] = y[i];
-            m0 = xreduce32<true>(t, lane);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) t[i] = y[32 + i];
-            m1 = xreduce32<true>(t, lane);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float ci = __shfl_sync(0xffffffffu, m0, i);
-              t[i] = ci == -INFINITY ? 0.f : ex2(y[i] - ci);
+            for (int i = 0; i < 64; ++i) {
+              const int ri = (i >> 5) * 2 + ((i >> 1) & 1);
+              const int col = cb + 8 * ((i >> 2) & 7) + 2 * t0 + (i & 1);
+              y[i] = (rok[ri] && col < p.ncols) ? y[i] * k2 : -INFINITY;
             }
-            S0 = xreduce32<false>(t, lane);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float ci = __shfl_sync(0xffffffffu, m1, i);
-              t[i] = ci == -INFINITY ? 0.f : ex2(y[32 + i] - ci);
+            for (int rho = 0; rho < 8; ++rho)
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+                cm[rho * 2 + c] = fmaxf(fmaxf(y[rho * 4 + c], y[rho * 4 + 2 + c]),
+                                        fmaxf(y[32 + rho * 4 + c], y[32 + rho * 4 + 2 + c]));
+#define XM16(O, N)                                                     \
+  {                                                                    \
+    const bool up = (lane & (O)) != 0;                                 \
+    _Pragma("unroll") for (int i = 0; i < (N); ++i) {                  \
+      const float send = up ? cm[i] : cm[i + (N)];                     \
+      const float keep = up ? cm[i + (N)] : cm[i];                     \
+      cm[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, (O)));    \
+    }                                                                  \
+  }
+            XM16(16, 8)
+            XM16(8, 4)
+            XM16(4, 2)
+#undef XM16
+            m0 = cm[0];
+            m1 = cm[1];
+#pragma unroll
+            for (int rho = 0; rho < 8; ++rho) {
+              const float c0 = __shfl_sync(0xffffffffu, m0, 4 * rho + t0);  // max of column 8rho+2t0
+              const float c1 = __shfl_sync(0xffffffffu, m1, 4 * rho + t0);  // max of column 8rho+2t0+1
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                const float cc = c ? c1 : c0;
+                float a = 0.f;
+                if (cc != -INFINITY) {
+                  a = ex2(y[rho * 4 + c] - cc) + ex2(y[rho * 4 + 2 + c] - cc) + ex2(y[32 + rho * 4 + c] - cc) +
+                      ex2(y[32 + rho * 4 + 2 + c] - cc);
+                }
+                P[rho * 2 + c] = a;
+              }
             }
-            S1 = xreduce32<false>(t, lane);
+#define XR16(O, N)                                                     \
+  {                                                                    \
+    const bool up = (lane & (O)) != 0;                                 \
+    _Pragma("unroll") for (int i = 0; i < (N); ++i) {                  \
+      const float send = up ? P[i] : P[i + (N)];                       \
+      const float keep = up ? P[i + (N)] : P[i];                       \
+      P[i] = keep + __shfl_xor_sync(0xffffffffu, send, (O));           \
+    }                                                                  \
+  }
+            XR16(16, 8)
+            XR16(8, 4)
+            XR16(4, 2)
+#undef XR16
+            S0 = P[0];
+            S1 = P[1];
           }
           // double-buffered S: release this buffer only after the (rare) exact fallback has re-read it
           tc_fence_before();
           named_bar_sync(1, 256);
           if (et == 0) mbar_arrive_cluster(&sfree[buf], 0);
-          xch[grp][rh][lane] = make_float2(m0, S0);
-          xch[grp][rh][32 + lane] = make_float2(m1, S1);
+          xch[grp][rh][2 * lane] = make_float2(m0, S0);
+          xch[grp][rh][2 * lane + 1] = make_float2(m1, S1);
           named_bar_sync(2 + grp, 64);
           if (rh == 0) {
-            float2 a0 = merge2(xch[grp][0][lane], xch[grp][1][lane]);
-            float2 a1 = merge2(xch[grp][0][32 + lane], xch[grp][1][32 + lane]);
+            float2 a0 = merge2(xch[grp][0][2 * lane], xch[grp][1][2 * lane]);
+            float2 a1 = merge2(xch[grp][0][2 * lane + 1], xch[grp][1][2 * lane + 1]);
             if (!first_visit) {
               a0 = merge2(pre0, a0);
               a1 = merge2(pre1, a1);
             }
-            if (cb + lane < p.ncols) slot[cb + lane] = a0;
-            if (cb + 32 + lane < p.ncols) slot[cb + 32 + lane] = a1;
+            if (cb + 2 * lane < p.ncols) slot[cb + 2 * lane] = a0;
+            if (cb + 2 * lane + 1 < p.ncols) slot[cb + 2 * lane + 1] = a1;
           }
         } else {
           // ---------------------------------------------------------- backward: G tile -> smem (bf16)
@@ -574,8 +673,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ++tile_ctr;
       }
       if constexpr (!BWD) {
-        // merge the 4 column slices of each row, write this segment's row partial
-        rowx[grp][r] = make_float2(m, sig);
+        // merge each row's 4 lane slices (t0), then its 4 column slices (h, u); write the segment's row partial
+        const int t0 = lane & 3, t1 = lane >> 2;
+#pragma unroll
+        for (int ri = 0; ri < 4; ++ri) {
+          float2 a = make_float2(mrow[ri], srow[ri]);
+#pragma unroll
+          for (int o = 1; o <= 2; o <<= 1) {
+            float2 bq;
+            bq.x = __shfl_xor_sync(0xffffffffu, a.x, o);
+            bq.y = __shfl_xor_sync(0xffffffffu, a.y, o);
+            a = merge2(a, bq);
+          }
+          if (t0 == 0) rowx[grp][rh * 32 + 16 * (ri >> 1) + 8 * (ri & 1) + t1] = a;
+        }
         named_bar_sync(1, 256);
         if (grp == 0 && row_ok) {
           float2 a = merge2(merge2(rowx[0][r], rowx[1][r]), merge2(rowx[2][r], rowx[3][r]));
@@ -613,7 +724,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (DBG && p.dbg && threadIdx.x == 0) atomicAdd(p.dbg + 4 * 16 + 15, (unsigned long long)(clock64() - t_start));
   tc_fence_before();
   cluster_sync();
-  if (warp == 1) tmem_dealloc<2>(tbase, kTmemCols);
+  if (warp == kWarpMMA) tmem_dealloc<2>(tbase, kTmemCols);
 }
 
 // ------------------------------------------------------------------------------------------ host side

@@ -122,6 +122,7 @@ extern "C" infcl_status infcl_probe_umma(const void* A, const void* B, int M, in
 // Operands resident in smem (contents irrelevant), one thread of the leader CTA issues `iters` back-to-back
 // MMAs of the given shape, then commits; cycles per MMA are measured on the issuing SM.
 namespace infcl {
+__device__ __forceinline__ bool lane_is_zero() { return (threadIdx.x & 31) == 0; }
 template <int NCTA>
 __global__ void __launch_bounds__(128, 1) probe_rate_kernel(int M, int N, int a_mn, int iters, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -144,37 +145,40 @@ __global__ void __launch_bounds__(128, 1) probe_rate_kernel(int M, int N, int a_
   if constexpr (NCTA == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tmem_base;
-  if (cta == 0 && threadIdx.x == 32) {
+  if (cta == 0 && warp == 1) {  // whole warp converged, elect.sync inside the asm (as in pair_kernel)
     const uint32_t idesc = idesc_bf16(M, N, a_mn & 1, 0);
     const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);
-    const long long t0 = clock64();
-    // a_mn >= 2 encodes a grouped loop: every G = a_mn >> 1 MMAs do a try_wait on a completed barrier, a
-    // tcgen05 fence and a commit (the pair kernel's per-stage overhead)
-    const int G = a_mn >= 2 ? (a_mn >> 1) : 0;
+    const int G = a_mn >= 2 ? (a_mn >> 1) : 0;  // every G MMAs: barrier wait + fence before, commit after
     const int amn = a_mn & 1;
-    for (int i = 0; i < iters; ++i) {
-      const int k = i & 3;
-      if (G && (i % G) == 0) {
+    const uint64_t ad0 = amn ? smem_desc_sw128(sa, 8192, 1024) : smem_desc_sw128(sa, 16, 1024);
+    const uint64_t bd0 = smem_desc_sw128(sb, 16, 1024);
+    const uint64_t astep = amn ? 128 : 2;
+    const long long t0 = clock64();
+    if (G == 0) {
+      for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) umma_bf16_warp<NCTA>(tbase, ad0 + (uint64_t)((k & 3) * astep), bd0 + (uint64_t)(2 * (k & 3)), idesc, 1u);
+      }
+    } else {
+      for (int i = 0; i < iters; i += 8) {
         mbar_wait(&bar_ready, 0);
         tc_fence_after();
-      }
-      uint64_t ad = amn ? smem_desc_sw128(sa + k * 2048, 8192, 1024) : smem_desc_sw128(sa + k * 32, 16, 1024);
-      uint64_t bd = smem_desc_sw128(sb + k * 32, 16, 1024);
-      umma_bf16<NCTA>(tbase, ad, bd, idesc, 1);
-      if (G && (i % G) == G - 1) {
-        if constexpr (NCTA == 2) umma_commit_pair_mc(&bar_dummy, 0x3);
-        else umma_commit_1cta(&bar_dummy);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) umma_bf16_warp<NCTA>(tbase, ad0 + (uint64_t)((k & 3) * astep), bd0 + (uint64_t)(2 * (k & 3)), idesc, 1u);
+        if constexpr (NCTA == 2) umma_commit_pair_mc_warp(&bar_dummy, 0x3);
       }
     }
     const long long t1 = clock64();
-    if constexpr (NCTA == 2) umma_commit_pair_mc(&bar_done, 0x3);
-    else umma_commit_1cta(&bar_done);
+    if constexpr (NCTA == 2) umma_commit_pair_mc_warp(&bar_done, 0x3);
+    else if (lane_is_zero()) umma_commit_1cta(&bar_done);
     mbar_wait(&bar_done, 0);
     const long long t2 = clock64();
-    out[0] = t1 - t0;
-    out[1] = t2 - t0;
+    if (threadIdx.x == 32) {
+      out[0] = t1 - t0;
+      out[1] = t2 - t0;
+    }
   }
-  if (cta != 0 || threadIdx.x != 32) mbar_wait(&bar_done, 0);
+  if (cta != 0 || warp != 1) mbar_wait(&bar_done, 0);
   tc_fence_before();
   if constexpr (NCTA == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) tmem_dealloc<NCTA>(tbase, 512);

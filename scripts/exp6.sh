@@ -1,0 +1,4 @@
+#!/bin/bash
+python -m pytest tests/test_gpu_parity.py -q -x --timeout 300 2>&1 | tail -2
+for D in 512 768; do TAG=warpprio D=$D python scripts/time_step.py; done
+INFCL_DEBUG_WAITS=1 python scripts/time_step.py 2>&1 | grep -E "total|role" | head -24

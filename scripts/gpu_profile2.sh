@@ -1,0 +1,9 @@
+#!/bin/bash
+TAG=${TAG:-r01}
+mkdir -p gpurun_out
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
+   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_bench_${TAG}.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pair_kernel -c 3 \
+   -o gpurun_out/prof_${TAG} -f python scripts/prof_step.py > gpurun_out/ncu_full_${TAG}.log 2>&1
+timeout 600 python bench.py --steps 40 --warmup 5 > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
+echo done

@@ -124,3 +124,11 @@ def make_features_device(b: int, d: int, seed: int, device, dtype=torch.bfloat16
     I = torch.nn.functional.normalize(I, dim=1).to(dtype)
     T = torch.nn.functional.normalize(T, dim=1).to(dtype)
     return I, T
+
+
+def make_onehot_device(b: int, d: int, K: int, device, dtype=torch.bfloat16):
+    """The ``onehot`` distribution built directly on a device (same values as make_features(..., dist="onehot"))."""
+    I = torch.zeros(b, d, device=device, dtype=dtype)
+    idx = torch.arange(b, device=device) % K
+    I[torch.arange(b, device=device), idx] = 1
+    return I, I.clone()

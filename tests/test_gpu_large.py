@@ -1,0 +1,105 @@
+"""Full-size parity (SURVEY.md 8(c) "large-b protocol"), in the launch configuration bench.py times.
+
+* cfg2 (b=65536, d=512, bf16, 1 GPU) on random paired inputs: every r_i, c_j and the loss against the exact fp64
+  oracle streamed over row chunks, and 256 stratified gradient rows of dI and dT against the exact fp64 rows
+  (oracle.sampled_row_grads with the oracle's own r, c).
+* cfg3 (b=262144, d=768) at n=1 and cfg4's per-rank workload (b=1048576, d=768 through the 8-rank virtual ring,
+  b_s = 131072) on structured inputs with closed forms (one-hot classes, codebook), exact at any b.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import make_features, make_onehot_device, codebook_assignment, codebook_vectors
+from paper_2410_17243_b200 import loss as K
+
+pytestmark = pytest.mark.gpu
+
+S = 14.2857
+
+
+def rel_norm(got, ref):
+    return np.linalg.norm(np.asarray(got, np.float64) - ref) / np.linalg.norm(ref)
+
+
+def stratified_rows(b, n=256, seed=0):
+    """Rows spread over 128-row tiles and positions within a tile (first/last rows of tiles included)."""
+    rng = np.random.default_rng(seed)
+    rows = set([0, 1, 63, 64, 127, 128, b - 1, b - 128, b - 129])
+    while len(rows) < n:
+        rows.add(int(rng.integers(0, b)))
+    return np.array(sorted(rows))
+
+
+def test_cfg2_full_size_random_paired():
+    b, d = 65536, 512
+    I, T = make_features(b, d, seed=1, dist="paired")
+    Id, Td = I.cuda(), T.cuda()
+    loss, r, c, dg = K.infcl_forward(Id, Td, b, S)
+    dI, dT = K.infcl_backward(Id, Td, b, S, r, c, dg, torch.tensor(1.0, device="cuda"))
+    torch.cuda.synchronize()
+    ref = oracle.streamed_forward(I, T, S, chunk=2048)
+    assert abs(loss.item() - ref["loss"]) <= 1e-4 * abs(ref["loss"])
+    assert np.abs(r.cpu().numpy() - ref["r"]).max() <= 2e-3
+    assert np.abs(c.cpu().numpy() - ref["c"]).max() <= 2e-3
+    assert np.abs(dg.cpu().numpy() - ref["diag"]).max() <= 2e-3
+    rows = stratified_rows(b)
+    rdI = oracle.sampled_row_grads(I, T, S, ref["r"], ref["c"], rows)
+    rdT = oracle.sampled_row_grads(T, I, S, ref["c"], ref["r"], rows)
+    assert rel_norm(dI.cpu().numpy()[rows], rdI) <= 2e-3
+    assert rel_norm(dT.cpu().numpy()[rows], rdT) <= 2e-3
+    # O(bd) identity over ALL rows: sum <dI_i, I_i> = sum <dT_j, T_j> (= s dL/ds)
+    a = (dI.double() * Id.double()).sum().item()
+    bb = (dT.double() * Td.double()).sum().item()
+    assert abs(a - bb) <= 1e-3 * max(abs(a), abs(bb), 1e-12)
+
+
+@pytest.mark.parametrize("b,d,world", [(262144, 768, 1), (1048576, 768, 8)])
+def test_large_onehot_closed_form(b, d, world):
+    """One-hot classes: r = c = log(m e^s + b - m), L = that - s, closed-form gradients (oracle.onehot_closed_form).
+    world=8 runs cfg4's exact per-rank shards (b_s = 131072) through the virtual 8-rank ring schedule."""
+    K_ = 512
+    s = 1.0  # well-conditioned gradient (DESIGN.md Tolerances)
+    Id, Td = make_onehot_device(b, d, K_, "cuda")
+    if world == 1:
+        loss, r, c, dg = K.infcl_forward(Id, Td, b, s)
+        dI, dT = K.infcl_backward(Id, Td, b, s, r, c, dg, torch.tensor(1.0, device="cuda"))
+    else:
+        loss, r, c, dg = K.infcl_forward_virtual(Id, Td, s, world)
+        dI, dT = K.infcl_backward_virtual(Id, Td, s, world, r, c, dg, torch.tensor(1.0, device="cuda"))
+    torch.cuda.synchronize()
+    m = b // K_
+    lam = float(np.log(m * np.exp(np.float32(s)) + (b - m)))
+    assert abs(loss.item() - (lam - float(np.float32(s)))) <= 1e-4 * abs(lam - s)
+    assert (r - lam).abs().max().item() <= 2e-3 and (c - lam).abs().max().item() <= 2e-3
+    rows = stratified_rows(b, 64)
+    # closed form per row (oracle.onehot_closed_form, evaluated for the sampled rows only): dI_i = s/b [ (m p - 1) e_k + m q sum_{k' != k} e_k' ],  p = e^{s - lam}, q = e^{-lam}
+    p = np.exp(np.float32(s) - lam)
+    q = np.exp(-lam)
+    s32 = float(np.float32(s))
+    want = np.zeros((len(rows), d))
+    want[:, :K_] = s32 / b * m * q
+    want[np.arange(len(rows)), rows % K_] = s32 / b * (m * p - 1.0)
+    assert rel_norm(dI.cpu().numpy()[rows], want) <= 2e-3
+    assert rel_norm(dT.cpu().numpy()[rows], want) <= 2e-3
+
+
+def test_cfg3_codebook_closed_form():
+    """Codebook inputs (K random unit codewords per side): exact r, c, loss and gradient rows at b = 262144."""
+    b, d, K_, seed = 262144, 768, 256, 5
+    I, T = make_features(b, d, seed=seed, dist="codebook", K=K_)
+    ci, ct = codebook_vectors(d, K_, seed)
+    ai, at = codebook_assignment(b, K_, seed)
+    Id, Td = I.cuda(), T.cuda()
+    del I, T
+    loss, r, c, dg = K.infcl_forward(Id, Td, b, S)
+    dI, dT = K.infcl_backward(Id, Td, b, S, r, c, dg, torch.tensor(1.0, device="cuda"))
+    torch.cuda.synchronize()
+    rows = stratified_rows(b, 128)
+    cf = oracle.codebook_closed_form(ci, ct, ai, at, S, rows=rows)
+    assert abs(loss.item() - cf["loss"]) <= 1e-4 * abs(cf["loss"])
+    assert np.abs(r.cpu().numpy() - cf["r"]).max() <= 2e-3
+    assert np.abs(c.cpu().numpy() - cf["c"]).max() <= 2e-3
+    assert rel_norm(dI.cpu().numpy()[rows], cf["dI"]) <= 2e-3
+    assert rel_norm(dT.cpu().numpy()[rows], cf["dT"]) <= 2e-3

@@ -24,3 +24,10 @@ def test_paired_correlated_and_shard():
     assert 0.6 < cos < 0.8
     parts = [shard(I, r, 4) for r in range(4)]
     assert torch.equal(torch.cat(parts), I)
+
+
+def test_onehot_device_matches_host():
+    from synth import make_onehot_device
+    I, T = make_features(300, 16, dist="onehot", K=8)
+    Id, Td = make_onehot_device(300, 16, 8, "cpu")
+    assert torch.equal(I, Id) and torch.equal(T, Td)
