@@ -329,10 +329,12 @@ def run_e2e(args, K, b, d, bs, s, rank, world, comm, dev):
     times = []
     if world == 1:
         scratch = torch.empty(int(K.L.lib().infcl_e2e_scratch_bytes(b, d, 0)), dtype=torch.uint8, device=dev)
-        K.infcl_loss_grad_host(Ih, Th, s, 1.0, scratch)
+        out = (torch.empty((), dtype=torch.float32).pin_memory(), torch.empty(b, d, dtype=torch.float32).pin_memory(),
+               torch.empty(b, d, dtype=torch.float32).pin_memory())
+        K.infcl_loss_grad_host(Ih, Th, s, 1.0, scratch, out)
         for _ in range(steps):
             t0 = time.perf_counter()
-            K.infcl_loss_grad_host(Ih, Th, s, 1.0, scratch)
+            K.infcl_loss_grad_host(Ih, Th, s, 1.0, scratch, out)
             times.append(time.perf_counter() - t0)
     else:
         ws = K.alloc_workspace(b, d, world, torch.bfloat16, dev)

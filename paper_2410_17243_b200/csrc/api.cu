@@ -407,10 +407,10 @@ extern "C" infcl_status infcl_forward(infcl_comm comm, const void* I_local, cons
   return INFCL_OK;
 }
 
-extern "C" infcl_status infcl_backward(infcl_comm comm, const void* I_local, const void* T_local, infcl_dtype dt,
-                                       int64_t b, int d, float s, int rank, int world, const float* row_lse,
-                                       const float* col_lse, const float* diag, const float* grad, float* dI,
-                                       float* dT, void* ws, size_t ws_bytes, void* stream) {
+static infcl_status backward_impl(infcl_comm comm, const void* I_local, const void* T_local, infcl_dtype dt,
+                                  int64_t b, int d, float s, int rank, int world, const float* row_lse,
+                                  const float* col_lse, const float* diag, const float* grad, float* dI, float* dT,
+                                  void* ws, size_t ws_bytes, void* stream, cudaEvent_t dI_ready) {
   const size_t need = infcl_workspace_bytes(b, d, world, dt);
   TRY(validate(I_local, T_local, dt, b, d, s, rank, world, ws, ws_bytes, need));
   if (!row_lse || !col_lse || !diag || !grad || !dI || !dT) return fail(INFCL_ERR_INVALID_ARG, "null pointer");
@@ -457,9 +457,18 @@ extern "C" infcl_status infcl_backward(infcl_comm comm, const void* I_local, con
       }
     }
     TRY(pass_end(R, pass, out, diag, row_lse, col_lse, grad, st));
+    if (pass == 0 && dI_ready) INFCL_CUDA_TRY(cudaEventRecord(dI_ready, st));  // dI final: callers may copy it out
   }
   INFCL_CUDA_TRY(cudaGetLastError());
   return INFCL_OK;
+}
+
+extern "C" infcl_status infcl_backward(infcl_comm comm, const void* I_local, const void* T_local, infcl_dtype dt,
+                                       int64_t b, int d, float s, int rank, int world, const float* row_lse,
+                                       const float* col_lse, const float* diag, const float* grad, float* dI,
+                                       float* dT, void* ws, size_t ws_bytes, void* stream) {
+  return backward_impl(comm, I_local, T_local, dt, b, d, s, rank, world, row_lse, col_lse, diag, grad, dI, dT, ws,
+                       ws_bytes, stream, nullptr);
 }
 
 // ------------------------------------------------------------------------------------------ virtual ring
@@ -606,11 +615,23 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
   INFCL_CUDA_TRY(cudaMemcpyAsync(T, T_host, (size_t)b * d * esz, cudaMemcpyHostToDevice, st));
   INFCL_CUDA_TRY(cudaMemcpyAsync(lg + 1, &grad_loss, sizeof(float), cudaMemcpyHostToDevice, st));
   TRY(infcl_forward(nullptr, I, T, dt, b, d, s, 0, 1, r, c, dg, lg, ws, wsb, stream));
-  TRY(infcl_backward(nullptr, I, T, dt, b, d, s, 0, 1, r, c, dg, lg + 1, dI, dT, ws, wsb, stream));
-  INFCL_CUDA_TRY(cudaMemcpyAsync(loss_host, lg, sizeof(float), cudaMemcpyDeviceToHost, st));
-  INFCL_CUDA_TRY(cudaMemcpyAsync(dI_host, dI, (size_t)b * d * 4, cudaMemcpyDeviceToHost, st));
+  // the dI device->host copy runs on a side stream while the dT pass computes
+  static cudaStream_t copy_stream = nullptr;
+  static cudaEvent_t ev_dI = nullptr, ev_fwd = nullptr;
+  if (!copy_stream) {
+    INFCL_CUDA_TRY(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    INFCL_CUDA_TRY(cudaEventCreateWithFlags(&ev_dI, cudaEventDisableTiming));
+    INFCL_CUDA_TRY(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
+  }
+  INFCL_CUDA_TRY(cudaEventRecord(ev_fwd, st));
+  INFCL_CUDA_TRY(cudaStreamWaitEvent(copy_stream, ev_fwd, 0));
+  INFCL_CUDA_TRY(cudaMemcpyAsync(loss_host, lg, sizeof(float), cudaMemcpyDeviceToHost, copy_stream));
+  TRY(backward_impl(nullptr, I, T, dt, b, d, s, 0, 1, r, c, dg, lg + 1, dI, dT, ws, wsb, stream, ev_dI));
+  INFCL_CUDA_TRY(cudaStreamWaitEvent(copy_stream, ev_dI, 0));
+  INFCL_CUDA_TRY(cudaMemcpyAsync(dI_host, dI, (size_t)b * d * 4, cudaMemcpyDeviceToHost, copy_stream));
   INFCL_CUDA_TRY(cudaMemcpyAsync(dT_host, dT, (size_t)b * d * 4, cudaMemcpyDeviceToHost, st));
   INFCL_CUDA_TRY(cudaStreamSynchronize(st));
+  INFCL_CUDA_TRY(cudaStreamSynchronize(copy_stream));
   return INFCL_OK;
 }
 

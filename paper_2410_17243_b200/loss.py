@@ -139,17 +139,21 @@ def infcl_backward_virtual(I, T, logit_scale: float, world: int, r, c, dg, grad_
 
 
 def infcl_loss_grad_host(I_host: torch.Tensor, T_host: torch.Tensor, logit_scale: float, grad_loss: float = 1.0,
-                         scratch: torch.Tensor | None = None):
-    """End-to-end call with HOST tensors (copies inside the library call); returns (loss, dI, dT) on host."""
+                         scratch: torch.Tensor | None = None, out=None):
+    """End-to-end call with HOST tensors (copies inside the library call); returns (loss, dI, dT) on host.
+    ``out`` = (loss, dI, dT) preallocated host tensors (pinned for full PCIe bandwidth) to reuse across calls."""
     b, d = I_host.shape
     dt = _dtype_code(I_host)
     n = int(L.lib().infcl_e2e_scratch_bytes(b, d, dt))
     if scratch is None or scratch.numel() < n:
         scratch = torch.empty(n, dtype=torch.uint8, device="cuda")
-    pin = I_host.is_pinned()
-    dI = torch.empty(b, d, dtype=torch.float32, pin_memory=pin)
-    dT = torch.empty_like(dI)
-    loss = torch.empty((), dtype=torch.float32)
+    if out is None:
+        pin = I_host.is_pinned()
+        dI = torch.empty(b, d, dtype=torch.float32, pin_memory=pin)
+        dT = torch.empty_like(dI)
+        loss = torch.empty((), dtype=torch.float32, pin_memory=pin)
+    else:
+        loss, dI, dT = out
     L.call("infcl_loss_grad_host", I_host.data_ptr(), T_host.data_ptr(), dt, b, d, float(logit_scale),
            float(grad_loss), loss.data_ptr(), dI.data_ptr(), dT.data_ptr(), scratch.data_ptr(), scratch.numel(),
            _stream())
