@@ -98,6 +98,17 @@ infcl_status infcl_backward(infcl_comm comm, const void* I_local, const void* T_
                             float* dT_local, void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------------------------
+ * infcl_grad_scale_partial -- g * dL/ds for a learnable logit scale (temperature, the
+ * CLIP convention of P:91's omitted temperature).  x_ij = s <I_i, T_j> is bilinear, so over the global batch
+ * s * dL/ds = sum_i <dI_i, I_i> exactly (pinned: tests/test_oracle_pins.py::test_scale_identity).
+ *   I_local [rows][d] (dtype dt), dI_local [rows][d] fp32 (this rank's infcl_backward output, already scaled
+ *   by g); out: device fp64 scalar, overwritten with sum_{i in shard} <dI_i, I_i> / s.  Callers sum the
+ *   partials over ranks (one scalar all-reduce).  s must be > 0 (INFCL_ERR_INVALID_ARG otherwise).
+ * ------------------------------------------------------------------------------------------------- */
+infcl_status infcl_grad_scale_partial(const void* I_local, const float* dI_local, infcl_dtype dt, int64_t rows, int d,
+                                      float logit_scale, double* out, void* stream);
+
+/* ---------------------------------------------------------------------------------------------------
  * Virtual ring (test/diagnostic): runs the same per-rank ring schedule for `world` logical ranks on ONE
  * device, exchanging blocks with device copies instead of NCCL.  Arguments are the full global batch:
  * I, T [b][d]; row_lse, col_lse, diag [b]; dI, dT [b][d].  Workspace: infcl_workspace_bytes(b, d, world, dt)

@@ -642,3 +642,16 @@ extern "C" void infcl_profile_enable(int on) { profile_enable(on != 0); }
 extern "C" infcl_status infcl_profile_read(int kind, int* launches, double* total_ms) {
   return profile_read(kind, launches, total_ms);
 }
+
+extern "C" infcl_status infcl_grad_scale_partial(const void* I_local, const float* dI_local, infcl_dtype dt,
+                                                 int64_t rows, int d, float s, double* out, void* stream) {
+  if (!I_local || !dI_local || !out) return fail(INFCL_ERR_INVALID_ARG, "null pointer");
+  if (dt != INFCL_BF16 && dt != INFCL_FP32) return fail(INFCL_ERR_INVALID_ARG, "bad dtype");
+  if (!(s > 0.f) || !std::isfinite(s)) return fail(INFCL_ERR_INVALID_ARG, "logit scale must be finite and > 0");
+  if (rows < 1 || d < 1) return fail(INFCL_ERR_SHAPE, "rows and d must be >= 1");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  INFCL_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
+  launch_grad_scale(I_local, dt == INFCL_FP32, dI_local, (long long)rows * d, 1.0 / (double)s, out, st);
+  INFCL_CUDA_TRY(cudaGetLastError());
+  return INFCL_OK;
+}

@@ -158,6 +158,32 @@ __global__ void combine_f32_kernel(const float* __restrict__ in, int ld_in, floa
   out[idx] = row[k] + row[(mode == 0 ? d : 2 * d) + k];
 }
 
+// sum_i <dI_i, I_i> * inv_s in fp64 (the logit-scale gradient identity)
+__global__ void grad_scale_kernel(const void* __restrict__ I, int i_f32, const float* __restrict__ dI, long long n,
+                                  double inv_s, double* out) {
+  double v = 0.0;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const float x = i_f32 ? reinterpret_cast<const float*>(I)[k]
+                          : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(I)[k]);
+    v += (double)x * (double)dI[k];
+  }
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __shared__ double ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) atomicAdd(out, v * inv_s);
+  }
+}
+
+void launch_grad_scale(const void* I, int i_f32, const float* dI, long long n, double inv_s, double* out,
+                       cudaStream_t s) {
+  grad_scale_kernel<<<std::min(nblk(n, 256), 1184u), 256, 0, s>>>(I, i_f32, dI, n, inv_s, out);
+  ++launch_counter();
+}
+
 void launch_init_state(float2* st, int n, cudaStream_t s) {
   init_state_kernel<<<nblk(n, 256), 256, 0, s>>>(st, n);
   ++launch_counter();

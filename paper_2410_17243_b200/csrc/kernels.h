@@ -57,6 +57,8 @@ void launch_diag_correction(float* dA, int ld_dA, const void* B, int ldB, int dt
                             const float* r, const float* c, const float* grad, float coef_base, float scale, int n,
                             int d, cudaStream_t s);
 void launch_split_f32(const float* x, void* out_bf16, int n, int d, int mode, cudaStream_t s);
+void launch_grad_scale(const void* I, int i_f32, const float* dI, long long n, double inv_s, double* out,
+                       cudaStream_t s);
 void launch_combine_f32(const float* in, int ld_in, float* out, int n, int d, int mode, cudaStream_t s);
 
 uint64_t& launch_counter();

@@ -74,6 +74,7 @@ struct KParams {
   float coef_base;
   unsigned long long* dbg;  // optional per-tag wait-cycle accumulators (INFCL_DEBUG_WAITS)
   int noepi;                // diagnostic: epilogue skips its math (results invalid; INFCL_DEBUG_NOEPI)
+  int notma;                // diagnostic: producer signals stages without loading (results invalid)
 };
 
 // Column-synchronous schedule.  Full waves: pair p owns row block w*P + p for w < W = n_rb / P and sweeps all
@@ -227,10 +228,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t ph = 0, aph = 0;
       auto load_stage = [&](int c0a, int c1a, int c0b, int c1b) {
         wc.wait(&empty[stage], ph ^ 1, 1);
-        if (cta == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStage);
-        uint8_t* dst = sStage + stage * kStage;
-        tma_load_2d_pair(dst, &tmB, &full[stage], c0a, c1a);
-        tma_load_2d_pair(dst + kBoxB, &tmB, &full[stage], c0b, c1b);
+        if (DBG && p.notma) {
+          if (cta == 0) mbar_arrive(&full[stage]);
+        } else {
+          if (cta == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStage);
+          uint8_t* dst = sStage + stage * kStage;
+          tma_load_2d_pair(dst, &tmB, &full[stage], c0a, c1a);
+          tma_load_2d_pair(dst + kBoxB, &tmB, &full[stage], c0b, c1b);
+        }
         if (++stage == p.n_stages) {
           stage = 0;
           ph ^= 1;
@@ -255,9 +260,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const long long seg_end = S.seg_end(it);
         wc.wait(&afree, aph ^ 1, 2);
         aph ^= 1;
-        if (cta == 0) mbar_arrive_expect_tx(&afull, 2u * p.KB * kBox);
-        for (int kb = 0; kb < p.KB; ++kb)
-          tma_load_2d_pair(sA + kb * kBox, &tmA, &afull, kb * 64, rb * kRowsPerPair + (int)cta * 64);
+        if (DBG && p.notma) {
+          if (cta == 0) mbar_arrive(&afull);
+        } else {
+          if (cta == 0) mbar_arrive_expect_tx(&afull, 2u * p.KB * kBox);
+          for (int kb = 0; kb < p.KB; ++kb)
+            tma_load_2d_pair(sA + kb * kBox, &tmA, &afull, kb * 64, rb * kRowsPerPair + (int)cta * 64);
+        }
         int prev = -1;
         for (; it < seg_end; ++it) {
           int rb_, ct;
@@ -314,6 +323,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         umma_commit_pair_mc_warp(&gfree, 0x3);
       };
+      const unsigned long long t_loop = DBG ? clock64() : 0ull;
       long long it = 0;
       while (it < nk) {
         const long long seg_end = S.seg_end(it);
@@ -329,6 +339,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t dS = tbase + buf * 128;
           for (int kc = 0; kc < p.KC; ++kc) {
             wc.wait(&full[stage], ph, 5);
+            const unsigned long long t_is = DBG ? clock64() : 0ull;
             tc_fence_after();
             const uint64_t ad0 = smem_desc_sw128(smem_u32(sA + 2 * kc * kBox), 16, 1024);
             const uint64_t bd0 = smem_desc_sw128(smem_u32(sStage + stage * kStage), 16, 1024);
@@ -342,10 +353,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                   bd0 + (uint64_t)((kBoxB >> 4) + 2 * (k & 3)), idS, 1u);
             }
             umma_commit_pair_mc_warp(&empty[stage], 0x3);
+            if (DBG) wc.acc[11] += clock64() - t_is;
             advance();
           }
+          const unsigned long long t_c = DBG ? clock64() : 0ull;
           umma_commit_pair_mc_warp(&sfull[buf], 0x3);
           if (it + 1 == seg_end) umma_commit_pair_mc_warp(&afree, 0x3);
+          if (DBG) wc.acc[10] += clock64() - t_c;
           ++tile_ctr;
           if (BWD) {
             if (have_prev) {
@@ -360,6 +374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           umma_commit_pair_mc_warp(&dafull, 0x3);
         }
       }
+      if (DBG) wc.acc[0] += clock64() - t_loop;
       wc.flush(1);
     }
   } else {
@@ -797,6 +812,7 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   if ((st = make_tmap_bf16(&tmB, a.B, a.ncols, a.dk, a.ld, 64, 128))) return st;
 
   k.noepi = getenv("INFCL_DEBUG_NOEPI") != nullptr;
+  k.notma = getenv("INFCL_DEBUG_NOTMA") != nullptr;
   auto kern = dbg_on ? pair_kernel<BWD, true> : pair_kernel<BWD, false>;
   INFCL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -817,8 +833,8 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
     cudaStreamSynchronize(s);
     const double nctas = 2.0 * g.npairs;
     fprintf(stderr, "[infcl dbg] %s kernel: mean cycles/CTA total=%.0f\n", BWD ? "BWD" : "FWD", h[4 * 16 + 15] / nctas);
-    const char* names[12] = {"-", "empty", "afree", "dafree", "gready", "full", "afull", "sfree", "sfull", "gfree",
-                             "dafull", "-"};
+    const char* names[12] = {"LOOP", "empty", "afree", "dafree", "gready", "full", "afull", "sfree", "sfull", "gfree",
+                             "dafull/sfull-commit", "S-issue"};
     for (int role = 0; role < 4; ++role)
       for (int t = 0; t < 12; ++t)
         if (h[role * 16 + t])

@@ -145,10 +145,29 @@ __global__ void __launch_bounds__(128, 1) probe_rate_kernel(int M, int N, int a_
   if constexpr (NCTA == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tmem_base;
+  __shared__ volatile int stop_flag;
+  if (threadIdx.x == 0) stop_flag = 0;
+  __syncthreads();
+  const int ld_mode = (a_mn >> 5) & 3;  // 1: warps 2-3 stream tcgen05.ld 16x256b; 2: 32x32b; from TMEM cols 256+
+  if (ld_mode && (warp == 2 || warp == 3)) {
+    float sink = 0.f;
+    float v[32];
+    while (!stop_flag) {
+#pragma unroll 1
+      for (int rep = 0; rep < 16; ++rep) {
+        const uint32_t ta = tbase + ((uint32_t)(warp * 32) << 16) + 256 + (rep & 3) * 32;
+        if (ld_mode == 1) tmem_ld16x256x8(ta, v);
+        else tmem_ld32(ta, v);
+        tmem_ld_wait();
+        sink += v[rep & 31];
+      }
+    }
+    if (sink == 12345.f) out[2] = 1;
+  }
   if (cta == 0 && warp == 1) {  // whole warp converged, elect.sync inside the asm (as in pair_kernel)
     const uint32_t idesc = idesc_bf16(M, N, a_mn & 1, 0);
     const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);
-    const int G = a_mn >= 2 ? (a_mn >> 1) : 0;  // every G MMAs: barrier wait + fence before, commit after
+    const int G = (a_mn & 31) >= 2 ? ((a_mn & 31) >> 1) : 0;  // every G MMAs: barrier wait + fence, commit
     const int amn = a_mn & 1;
     const uint64_t ad0 = amn ? smem_desc_sw128(sa, 8192, 1024) : smem_desc_sw128(sa, 16, 1024);
     const uint64_t bd0 = smem_desc_sw128(sb, 16, 1024);
@@ -173,11 +192,13 @@ __global__ void __launch_bounds__(128, 1) probe_rate_kernel(int M, int N, int a_
     else if (lane_is_zero()) umma_commit_1cta(&bar_done);
     mbar_wait(&bar_done, 0);
     const long long t2 = clock64();
-    if (threadIdx.x == 32) {
+    if (threadIdx.x == 32 && blockIdx.x == 0) {
       out[0] = t1 - t0;
       out[1] = t2 - t0;
     }
+    stop_flag = 1;
   }
+  if (NCTA == 2 && cta != 0 && threadIdx.x == 0) stop_flag = 1;
   if (cta != 0 || warp != 1) mbar_wait(&bar_done, 0);
   tc_fence_before();
   if constexpr (NCTA == 2) cluster_sync(); else __syncthreads();
@@ -189,7 +210,9 @@ extern "C" infcl_status infcl_probe_mma_rate(int M, int N, int a_mn_major, int n
                                              void* stream) {
   if (!out_cycles || (ncta != 1 && ncta != 2) || iters < 1) return fail(INFCL_ERR_INVALID_ARG, "bad probe args");
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ncta);
+  const int nclusters = (a_mn_major >> 8) > 0 ? (a_mn_major >> 8) : 1;  // bits 8+: clusters launched concurrently
+  a_mn_major &= 0xff;
+  cfg.gridDim = dim3(ncta * nclusters);
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = 64 * 1024 + 1024;
   cfg.stream = (cudaStream_t)stream;

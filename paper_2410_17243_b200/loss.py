@@ -109,6 +109,20 @@ def infcl_backward(I_local, T_local, b: int, logit_scale: float, row_lse, col_ls
     return dI, dT
 
 
+def infcl_grad_scale(I_local, dI_local, logit_scale: float, group=None):
+    """g * dL/ds (learnable temperature): sum_i <dI_i, I_i> / s over the global batch (include/infcl.h).
+    The per-rank partial is summed with torch.distributed when a process group is initialised."""
+    I_local = I_local.contiguous()
+    dI_local = dI_local.contiguous()
+    out = torch.empty((), device=I_local.device, dtype=torch.float64)
+    L.call("infcl_grad_scale_partial", I_local.data_ptr(), dI_local.data_ptr(), _dtype_code(I_local),
+           I_local.shape[0], I_local.shape[1], float(logit_scale), out.data_ptr(), _stream())
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(out, group=group)
+    return out
+
+
 def infcl_forward_virtual(I, T, logit_scale: float, world: int):
     """Whole batch on one device, ring schedule over `world` logical ranks (test of the ring engine)."""
     I, T = _check_features(I, T)

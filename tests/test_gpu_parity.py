@@ -181,3 +181,23 @@ def test_forward_exact_fallback_adversarial_columns():
     I = I.to(torch.bfloat16)
     T = T.to(torch.bfloat16)
     check_all(I, T, 100.0)
+
+
+@pytest.mark.parametrize("s", [1.0, 14.2857, 100.0])
+def test_grad_scale(s):
+    """g dL/ds via the bilinearity identity s dL/ds = sum_i <dI_i, I_i> against the oracle's direct
+    sum_ij G_ij <I_i, T_j>."""
+    b, d = 2048, 256
+    I, T = make_features(b, d, seed=13, dist="paired")
+    Id, Td = I.cuda(), T.cuda()
+    loss, r, c, dg = K.infcl_forward(Id, Td, b, s)
+    dI, dT = K.infcl_backward(Id, Td, b, s, r, c, dg, torch.tensor(0.7, device="cuda"))
+    ds = K.infcl_grad_scale(Id, dI, s).item()
+    _, _, ref = oracle.backward(I, T, s, 0.7, want_ds=True)
+    aI, _ = oracle.backward_abs(I, T, s, 0.7)
+    # |d ds| <= |sum_i <d dI_i, I_i>| / s <= ||d dI|| ||I|| / s: gate from the gradient gate
+    # gradient gate incl. its absolute floor 1e-6 max(s,1)|g| per element (check_all), mapped through |<dI, I>| / s
+    dI_err = GRAD_RTOL * np.linalg.norm(oracle.backward(I, T, s, 0.7)[0]) + U_G * np.linalg.norm(aI) \
+        + 1e-6 * max(s, 1.0) * 0.7 * np.sqrt(b * d)
+    tol = dI_err * np.linalg.norm(oracle.to_f64(I)) / s
+    assert abs(ds - ref) <= tol, (ds, ref, tol)
