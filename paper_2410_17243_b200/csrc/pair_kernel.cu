@@ -179,7 +179,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* sStage = sG + (BWD ? 4 * kBox : 0);
 
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
-  __shared__ __align__(8) uint64_t afull, afree, sfull[2], sfree[2], gready, gfree, dafull, dafree;
+  constexpr int kNB = BWD ? 1 : 4;  // S buffers in TMEM (forward: 4 x 128 columns, MMA runs up to 3 tiles ahead)
+  __shared__ __align__(8) uint64_t afull, afree, sfull[kNB], sfree[kNB], gready, gfree, dafull, dafree;
   __shared__ uint32_t tmem_base;
   __shared__ __align__(16) float2 xch[4][2][64];  // forward column partials of the 2 warps of a group
   __shared__ float2 rowx[4][64];                  // forward row partials of the 4 column slices
@@ -190,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int pair = blockIdx.x >> 1;
   const Sched S(p.n_rb, p.n_ct, p.npairs, pair);
   const long long nk = S.n_local();
-  constexpr uint32_t kTmemCols = BWD ? 512 : 256;
+  constexpr uint32_t kTmemCols = 512;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.n_stages; ++s) {
@@ -199,9 +200,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     mbar_init(&afull, 1);
     mbar_init(&afree, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kNB; ++b) {
       mbar_init(&sfull[b], 1);
-      mbar_init(&sfree[b], 2);
+      mbar_init(&sfree[b], 16);  // one arrival per epilogue warp of both CTAs
     }
     mbar_init(&gready, 2);
     mbar_init(&gfree, 1);
@@ -286,7 +287,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       WaitClock<DBG> wc(lane == 0 ? p.dbg : nullptr);
       int stage = 0;
       uint32_t ph = 0, aph = 0, gph = 0, dph = 0;
-      uint32_t sfph[2] = {0, 0};
+      uint32_t sfph[kNB] = {};
       int tile_ctr = 0;
       const uint32_t idS = idesc_bf16(128, 256, 0, 0);
       const uint32_t idD = idesc_bf16(256, 128, 1, 0);
@@ -332,7 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_after();
         bool have_prev = false, first_dA = true;
         for (; it < seg_end; ++it) {
-          const int buf = BWD ? 0 : (tile_ctr & 1);
+          const int buf = BWD ? 0 : (tile_ctr & (kNB - 1));
           wc.wait(&sfree[buf], sfph[buf] ^ 1, 7, true);
           sfph[buf] ^= 1;
           tc_fence_after();
@@ -390,7 +391,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int grp = h * 2 + u;     // the 2 warps (rh = 0, 1) that share these 64 columns
     const int et = ep * 32 + lane;  // 0..255
     const uint32_t laddr = tbase + ((uint32_t)(q * 32) << 16) + u * 64;
-    uint32_t sph[2] = {0, 0}, gfph = 0, daph = 0;
+    uint32_t sph[kNB] = {}, gfph = 0, daph = 0;
     WaitClock<DBG> wc(lane == 0 ? p.dbg : nullptr);
     int tile_ctr = 0;
     const float k2 = p.k2;
@@ -416,7 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (; it < seg_end; ++it) {
         int rb_, ct;
         S.decode(it, rb_, ct);
-        const int buf = BWD ? 0 : (tile_ctr & 1);
+        const int buf = BWD ? 0 : (tile_ctr & (kNB - 1));
         const int cb = ct * kColsPerTile + h * 128 + u * 64;  // global column of this thread's column 0
         const bool diag_tile = p.diag_on && ig >= cb && ig < cb + 64;
         const bool clean = row_ok && (cb + 64 <= p.ncols) && !diag_tile;
@@ -446,17 +447,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tmem_ld16x256x8(laddr + (16u << 16) + buf * 128, v + 32);
         }
         tmem_ld_wait();
-        if constexpr (BWD) {  // single S buffer: release it as soon as it is in registers
+        if constexpr (BWD) {  // single S buffer: each warp releases it as soon as its slice is in registers
           tc_fence_before();
-          named_bar_sync(1, 256);
-          if (et == 0) mbar_arrive_cluster(&sfree[buf], 0);
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(&sfree[buf], 0);
         }
 
         if (DBG && p.noepi) {
           if (!BWD) {
             tc_fence_before();
-            named_bar_sync(1, 256);
-            if (et == 0) mbar_arrive_cluster(&sfree[buf], 0);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(&sfree[buf], 0);
           } else {
             wc.wait(&gfree, gfph ^ 1, 9);
             gfph ^= 1;
@@ -633,10 +634,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             S0 = P[0];
             S1 = P[1];
           }
-          // double-buffered S: release this buffer only after the (rare) exact fallback has re-read it
+          // release this S buffer (per warp) only after the (rare) exact fallback has re-read it
           tc_fence_before();
-          named_bar_sync(1, 256);
-          if (et == 0) mbar_arrive_cluster(&sfree[buf], 0);
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(&sfree[buf], 0);
           xch[grp][rh][2 * lane] = make_float2(m0, S0);
           xch[grp][rh][2 * lane + 1] = make_float2(m1, S1);
           named_bar_sync(2 + grp, 64);

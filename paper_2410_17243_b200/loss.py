@@ -176,23 +176,30 @@ def infcl_loss_grad_host(I_host: torch.Tensor, T_host: torch.Tensor, logit_scale
 
 class _InfCLFunction(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, I_local, T_local, b, logit_scale, rank, world, comm):
+    def forward(ctx, I_local, T_local, scale_t, b, logit_scale, rank, world, comm):
         loss, r, c, dg = infcl_forward(I_local, T_local, b, logit_scale, rank, world, comm)
         ctx.save_for_backward(I_local, T_local, r, c, dg)
-        ctx.meta = (b, logit_scale, rank, world, comm)
+        ctx.meta = (b, logit_scale, rank, world, comm, scale_t is not None and scale_t.requires_grad)
         return loss
 
     @staticmethod
     def backward(ctx, grad_out):
         I_local, T_local, r, c, dg = ctx.saved_tensors
-        b, s, rank, world, comm = ctx.meta
+        b, s, rank, world, comm, want_ds = ctx.meta
         dI, dT = infcl_backward(I_local, T_local, b, s, r, c, dg, grad_out, rank, world, comm)
-        return dI.to(I_local.dtype), dT.to(T_local.dtype), None, None, None, None, None
+        ds = None
+        if want_ds:  # g * dL/ds = sum_i <dI_i, I_i> / s over the global batch (include/infcl.h)
+            ds = infcl_grad_scale(I_local, dI, s).to(torch.float32)
+        return dI.to(I_local.dtype), dT.to(T_local.dtype), ds, None, None, None, None, None
 
 
-def infcl_loss(I_local: torch.Tensor, T_local: torch.Tensor, logit_scale: float, comm: RingComm | None = None):
-    """Symmetric InfoNCE loss L = (L_I + L_T)/2 over the global batch (this rank's shards), differentiable."""
+def infcl_loss(I_local: torch.Tensor, T_local: torch.Tensor, logit_scale, comm: RingComm | None = None):
+    """Symmetric InfoNCE loss L = (L_I + L_T)/2 over the global batch (this rank's shards), differentiable in
+    I_local, T_local and -- when ``logit_scale`` is a tensor that requires grad (CLIP's learnable temperature,
+    the scale itself, not its log) -- in the logit scale."""
     world = comm.world if comm is not None else 1
     rank = comm.rank if comm is not None else 0
     b = I_local.shape[0] * world
-    return _InfCLFunction.apply(I_local, T_local, b, float(logit_scale), rank, world, comm)
+    scale_t = logit_scale if isinstance(logit_scale, torch.Tensor) else None
+    s = float(logit_scale.detach()) if scale_t is not None else float(logit_scale)
+    return _InfCLFunction.apply(I_local, T_local, scale_t, b, s, rank, world, comm)

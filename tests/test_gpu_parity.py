@@ -201,3 +201,14 @@ def test_grad_scale(s):
         + 1e-6 * max(s, 1.0) * 0.7 * np.sqrt(b * d)
     tol = dI_err * np.linalg.norm(oracle.to_f64(I)) / s
     assert abs(ds - ref) <= tol, (ds, ref, tol)
+
+
+def test_autograd_learnable_scale():
+    I, T = make_features(512, 128, seed=6)
+    Id = I.cuda().requires_grad_(True)
+    Td = T.cuda().requires_grad_(True)
+    s = torch.tensor(14.2857, device="cuda", requires_grad=True)
+    loss = K.infcl_loss(Id, Td, s)
+    loss.backward()
+    _, _, ref = oracle.backward(I, T, 14.2857, 1.0, want_ds=True)
+    assert abs(s.grad.item() - ref) <= 2e-3 * abs(ref) + 1e-6, (s.grad.item(), ref)
