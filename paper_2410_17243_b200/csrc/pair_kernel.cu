@@ -184,7 +184,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base;
   __shared__ __align__(16) float2 xch[4][2][64];  // forward column partials of the 2 warps of a group
   __shared__ float2 rowx[4][64];                  // forward row partials of the 4 column slices
-  __shared__ __align__(16) float cval[2][256];    // backward column LSEs (log2), double-buffered
+  __shared__ __align__(16) float cval[8][64];     // backward: each warp's 64 column LSEs (log2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = cluster_ctarank();
@@ -204,10 +204,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&sfull[b], 1);
       mbar_init(&sfree[b], 16);  // one arrival per epilogue warp of both CTAs
     }
-    mbar_init(&gready, 2);
+    mbar_init(&gready, 16);
     mbar_init(&gfree, 1);
     mbar_init(&dafull, 1);
-    mbar_init(&dafree, 2);
+    mbar_init(&dafree, 16);
     fence_mbar_init();
   }
   if (warp == kWarpTMA && lane == 0) {
@@ -399,15 +399,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (BWD) {
       coef = p.coef_base * __ldg(p.grad);
     }
+    // backward: this warp's column LSEs for the next tile, prefetched into registers one tile ahead
+    // (lane l holds columns 2l, 2l+1 of the warp's 64-column slice) -> no cross-warp barrier per tile
+    float2 pc = make_float2(0.f, 0.f);
+    auto load_pc = [&](long long item) {
+      int rbn, ctn;
+      S.decode(item, rbn, ctn);
+      const int j = ctn * kColsPerTile + h * 128 + u * 64 + 2 * lane;
+      pc.x = j < p.ncols ? __ldg(p.lse_col2 + j) : 0.f;
+      pc.y = j + 1 < p.ncols ? __ldg(p.lse_col2 + j + 1) : 0.f;
+    };
+    if (BWD && nk > 0) load_pc(0);
     long long it = 0;
     while (it < nk) {
       int rb, ct_first;
       S.decode(it, rb, ct_first);
       const long long seg_end = S.seg_end(it);
-      if (BWD) {  // column LSEs of the segment's first tile (later tiles are prefetched one tile ahead)
-        const int j = ct_first * kColsPerTile + et;
-        cval[tile_ctr & 1][et] = j < p.ncols ? __ldg(p.lse_col2 + j) : 0.f;
-      }
       const int ig = rb * kRowsPerPair + (int)cta * 64 + r;
       const bool row_ok = ig < p.nrows;
       // forward (16x256b layout): running (m, sigma) of this thread's 4 rows over its 16-column slice
@@ -421,12 +428,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int cb = ct * kColsPerTile + h * 128 + u * 64;  // global column of this thread's column 0
         const bool diag_tile = p.diag_on && ig >= cb && ig < cb + 64;
         const bool clean = row_ok && (cb + 64 <= p.ncols) && !diag_tile;
-        float pre_c = 0.f;  // backward: next tile's column LSE (prefetch)
-        if (BWD && it + 1 < seg_end) {
-          int rbn, ctn;
-          S.decode(it + 1, rbn, ctn);
-          const int j = ctn * kColsPerTile + et;
-          pre_c = j < p.ncols ? __ldg(p.lse_col2 + j) : 0.f;
+        if (BWD) {  // publish this tile's column LSEs to the warp's slot, then prefetch the next tile's
+          *reinterpret_cast<float2*>(&cval[ep][2 * lane]) = pc;
+          __syncwarp();
+          if (it + 1 < nk) load_pc(it + 1);
         }
         float2 pre0 = make_float2(-INFINITY, 0.f), pre1 = pre0;  // forward: slot values (prefetch)
         const bool first_visit = it < p.n_ct;
@@ -462,8 +467,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             wc.wait(&gfree, gfph ^ 1, 9);
             gfph ^= 1;
             fence_proxy_async_smem();
-            named_bar_sync(1, 256);
-            if (et == 0) mbar_arrive_cluster(&gready, 0);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(&gready, 0);
           }
         } else if constexpr (!BWD) {
           // ---------------------------------------------------------- forward statistics
@@ -653,7 +658,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         } else {
           // ---------------------------------------------------------- backward: G tile -> smem (bf16)
-          const float* cv = cval[tile_ctr & 1] + h * 128 + u * 64;
+          const float* cv = cval[ep];
           uint32_t pk[32];
 #pragma unroll
           for (int j = 0; j < 64; j += 4) {
@@ -681,10 +686,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int c16 = 0; c16 < 8; ++c16)
             st_shared_v4(gb + ((c16 ^ (r & 7)) << 4), pk[c16 * 4 + 0], pk[c16 * 4 + 1], pk[c16 * 4 + 2],
                          pk[c16 * 4 + 3]);
-          if (it + 1 < seg_end) cval[(tile_ctr + 1) & 1][et] = pre_c;
           fence_proxy_async_smem();
-          named_bar_sync(1, 256);
-          if (et == 0) mbar_arrive_cluster(&gready, 0);
+          __syncwarp();  // all G writes of this warp done (and cval reads before the next tile's rewrite)
+          if (lane == 0) mbar_arrive_cluster(&gready, 0);
         }
         ++tile_ctr;
       }
@@ -730,8 +734,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         tc_fence_before();
-        named_bar_sync(1, 256);
-        if (et == 0) mbar_arrive_cluster(&dafree, 0);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&dafree, 0);
       }
     }
     wc.flush(2 + (ep & 1));
