@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libinfcl.so")
+# INFCL_LIB: an A/B build variant of the same sources (scripts/build_variant.py); never a different implementation
+LIB_PATH = os.environ.get("INFCL_LIB") or os.path.join(_HERE, "libinfcl.so")
 
 INFCL_BF16 = 0
 INFCL_FP32 = 1

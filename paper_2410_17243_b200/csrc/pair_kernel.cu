@@ -143,9 +143,12 @@ __device__ __forceinline__ float xreduce32(float (&t)[32], int lane) {
 
 template <bool ON>
 struct WaitClock {
+  // every lane of the role times its waits (a lane-dependent branch here would diverge a converged warp and
+  // hide the wait of the lanes that did not time); only lane 0 flushes
   unsigned long long* dbg;
+  bool leader;
   unsigned long long acc[ON ? 12 : 1];
-  __device__ WaitClock(unsigned long long* d) : dbg(d) {
+  __device__ WaitClock(unsigned long long* d, bool lead) : dbg(d), leader(lead) {
 #pragma unroll
     for (int i = 0; i < (ON ? 12 : 1); ++i) acc[i] = 0;
   }
@@ -161,7 +164,7 @@ struct WaitClock {
     acc[tag] += clock64() - t0;
   }
   __device__ void flush(int role) {
-    if (!ON || !dbg) return;
+    if (!ON || !dbg || !leader) return;
     for (int i = 0; i < 12; ++i)
       if (acc[i]) atomicAdd(dbg + role * 16 + i, acc[i]);
   }
@@ -224,7 +227,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == kWarpTMA) {
     // ===================================================================== TMA producer (both CTAs)
     if (lane == 0) {
-      WaitClock<DBG> wc(lane == 0 ? p.dbg : nullptr);
+      WaitClock<DBG> wc(p.dbg, lane == 0);
       int stage = 0;
       uint32_t ph = 0, aph = 0;
       auto load_stage = [&](int c0a, int c1a, int c0b, int c1b) {
@@ -284,7 +287,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================================================================== MMA issuer (leader CTA)
     // the whole warp runs converged (warp-uniform descriptors); elect.sync inside the asm issues
     if (cta == 0) {
-      WaitClock<DBG> wc(lane == 0 ? p.dbg : nullptr);
+      WaitClock<DBG> wc(p.dbg, lane == 0);
       int stage = 0;
       uint32_t ph = 0, aph = 0, gph = 0, dph = 0;
       uint32_t sfph[kNB] = {};
@@ -392,7 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int et = ep * 32 + lane;  // 0..255
     const uint32_t laddr = tbase + ((uint32_t)(q * 32) << 16) + u * 64;
     uint32_t sph[kNB] = {}, gfph = 0, daph = 0;
-    WaitClock<DBG> wc(lane == 0 ? p.dbg : nullptr);
+    WaitClock<DBG> wc(p.dbg, lane == 0);
     int tile_ctr = 0;
     const float k2 = p.k2;
     float coef = 0.f;
@@ -516,28 +519,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               for (int c = 0; c < 2; ++c) mv = fmaxf(mv, v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + c]);
             ml[ri] = mv == -INFINITY ? -INFINITY : mv * k2;
           }
-          // shared exponentials E = 2^{y - ml} (y = v * s * log2 e), row sums
+          // shared exponentials E = 2^{y - ml} (y = v * s * log2 e), row sums. Branch-free so the 4 rows'
+          // exponentials interleave: an all-masked row uses reference 0 and its -inf logits give E = 0.
 #pragma unroll
           for (int ri = 0; ri < 4; ++ri) {
-            float acc = 0.f;
-            if (ml[ri] != -INFINITY) {
+            const float ref = ml[ri] == -INFINITY ? 0.f : ml[ri];
+            float part[8];
 #pragma unroll
-              for (int rho = 0; rho < 8; ++rho)
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                  float& x = v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + c];
-                  x = ex2(fmaf(x, k2, -ml[ri]));
-                  acc += x;
-                }
-              const float mn = fmaxf(mrow[ri], ml[ri]);
-              srow[ri] = srow[ri] * ex2(mrow[ri] - mn) + acc * ex2(ml[ri] - mn);
-              mrow[ri] = mn;
-            } else {
-#pragma unroll
-              for (int rho = 0; rho < 8; ++rho)
-#pragma unroll
-                for (int c = 0; c < 2; ++c) v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + c] = 0.f;
+            for (int rho = 0; rho < 8; ++rho) {
+              float& x0 = v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2];
+              float& x1 = v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + 1];
+              x0 = ex2(fmaf(x0, k2, -ref));
+              x1 = ex2(fmaf(x1, k2, -ref));
+              part[rho] = x0 + x1;
             }
+            const float acc = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
+            const float mn = fmaxf(mrow[ri], ml[ri]);
+            const float a_old = mrow[ri] == -INFINITY ? 0.f : ex2(mrow[ri] - mn);
+            const float a_new = ml[ri] == -INFINITY ? 0.f : ex2(ml[ri] - mn);
+            srow[ri] = srow[ri] * a_old + acc * a_new;
+            mrow[ri] = mn;
           }
           float Rw = fmaxf(fmaxf(ml[0], ml[1]), fmaxf(ml[2], ml[3]));
 #pragma unroll

@@ -48,11 +48,20 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// INFCL_TRYWAIT_HINT: optional suspend-time hint (ns) of try_wait; with a hint ptxas inserts NANOSLEEP.SYNCS
+// between probes, without one the probe loop spins on SYNCS.PHASECHK.TRYWAIT (A/B: scripts/build_variant.py)
+#ifdef INFCL_TRYWAIT_HINT
+#define INFCL_TW_SUFFIX ", " INFCL_STR(INFCL_TRYWAIT_HINT)
+#else
+#define INFCL_TW_SUFFIX ""
+#endif
+#define INFCL_STR2(x) #x
+#define INFCL_STR(x) INFCL_STR2(x)
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2" INFCL_TW_SUFFIX ";\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(addr), "r"(parity)
@@ -64,7 +73,7 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t pa
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2" INFCL_TW_SUFFIX ";\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(addr), "r"(parity)
