@@ -53,12 +53,12 @@ constexpr int kThreads = 320;  // warps 0-7 epilogue, warp 8 TMA, warp 9 MMA
 constexpr int kWarpTMA = 8, kWarpMMA = 9;
 constexpr int kBox = 8192;     // A_R / G block: 64 rows x 64 bf16 (128 B, SW128)
 constexpr int kBoxB = 16384;   // streamed B box: 128 rows x 64 bf16 (128 B, SW128)
-constexpr int kStage = 32768;  // one ring stage: two B boxes (8 MMAs per barrier round trip)
-constexpr int kMaxStages = 12;
+constexpr int kMaxStages = 16;
 
 struct KParams {
   int nrows, ncols, dk, KB, KC, NDC;
   int n_rb, n_ct, npairs, n_stages;
+  int sbox, stage_bytes;  // B boxes per ring stage (forward 1 = 16 KB stages, backward 2 = 32 KB) and its bytes
   long long n_items;
   float k2, scale;
   int diag_on;
@@ -185,7 +185,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   constexpr int kNB = BWD ? 1 : 4;  // S buffers in TMEM (forward: 4 x 128 columns, MMA runs up to 3 tiles ahead)
   __shared__ __align__(8) uint64_t afull, afree, sfull[kNB], sfree[kNB], gready, gfree, dafull, dafree;
   __shared__ uint32_t tmem_base;
-  __shared__ __align__(16) float2 xch[4][2][64];  // forward column partials of the 2 warps of a group
+  __shared__ __align__(16) float2 xch[2][4][2][64];  // forward column partials of a group's 2 warps (x tile parity)
   __shared__ float2 rowx[4][64];                  // forward row partials of the 4 column slices
   __shared__ __align__(16) float cval[8][64];     // backward: each warp's 64 column LSEs (log2)
 
@@ -235,20 +235,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (DBG && p.notma) {
           if (cta == 0) mbar_arrive(&full[stage]);
         } else {
-          if (cta == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStage);
-          uint8_t* dst = sStage + stage * kStage;
+          if (cta == 0) mbar_arrive_expect_tx(&full[stage], 2 * p.stage_bytes);
+          uint8_t* dst = sStage + stage * p.stage_bytes;
           tma_load_2d_pair(dst, &tmB, &full[stage], c0a, c1a);
-          tma_load_2d_pair(dst + kBoxB, &tmB, &full[stage], c0b, c1b);
+          if (BWD || p.sbox == 2) tma_load_2d_pair(dst + kBoxB, &tmB, &full[stage], c0b, c1b);
         }
         if (++stage == p.n_stages) {
           stage = 0;
           ph ^= 1;
         }
       };
-      // S stage kc: this CTA's 128 columns j, d-blocks 2kc and 2kc+1 (K-major operand, K = d)
+      // S stage kc: this CTA's 128 columns j, d-blocks sbox*kc (and sbox*kc + 1) (K-major operand, K = d)
       auto load_S = [&](int ct) {
         const int j0 = ct * kColsPerTile + (int)cta * 128;
-        for (int kc = 0; kc < p.KC; ++kc) load_stage(kc * 128, j0, kc * 128 + 64, j0);
+        const int sb = BWD ? 2 : p.sbox;
+        for (int kc = 0; kc < p.KC; ++kc) load_stage(kc * sb * 64, j0, kc * sb * 64 + 64, j0);
       };
       // dA stage (tc, jc): 128 columns j of the tile, this CTA's 128 d-rows of chunk tc (MN-major operand, K = j)
       auto load_dA = [&](int ct) {
@@ -272,9 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tma_load_2d_pair(sA + kb * kBox, &tmA, &afull, kb * 64, rb * kRowsPerPair + (int)cta * 64);
         }
         int prev = -1;
-        for (; it < seg_end; ++it) {
-          int rb_, ct;
-          S.decode(it, rb_, ct);
+        for (int ct = ct0; it < seg_end; ++it, ++ct) {  // a segment's column tiles are consecutive
           load_S(ct);
           if (BWD && prev >= 0) load_dA(prev);
           prev = ct;
@@ -290,7 +289,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       WaitClock<DBG> wc(p.dbg, lane == 0);
       int stage = 0;
       uint32_t ph = 0, aph = 0, gph = 0, dph = 0;
-      uint32_t sfph[kNB] = {};
+      uint32_t sfph = 0;  // phase bit of sfree[b] = bit b (a register, not a dynamically indexed array)
       int tile_ctr = 0;
       const uint32_t idS = idesc_bf16(128, 256, 0, 0);
       const uint32_t idD = idesc_bf16(256, 128, 1, 0);
@@ -313,7 +312,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             wc.wait(&full[stage], ph, 5);
             tc_fence_after();
             // descriptors advance by adding (byte offset >> 4) to the start-address field
-            const uint64_t ad0 = smem_desc_sw128(smem_u32(sStage + stage * kStage), kBoxB, 1024);  // MN-major B_C^T
+            const uint64_t ad0 = smem_desc_sw128(smem_u32(sStage + stage * p.stage_bytes), kBoxB, 1024);  // MN-major B_C^T
             const uint64_t bd0 = smem_desc_sw128(smem_u32(sG + jc * 2 * kBox), 16, 1024);           // K-major G
             const uint32_t dD = tbase + 128 + tc * 128;
             umma_bf16_warp<2>(dD, ad0, bd0, idD, (first && jc == 0) ? 0u : 1u);
@@ -337,20 +336,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         bool have_prev = false, first_dA = true;
         for (; it < seg_end; ++it) {
           const int buf = BWD ? 0 : (tile_ctr & (kNB - 1));
-          wc.wait(&sfree[buf], sfph[buf] ^ 1, 7, true);
-          sfph[buf] ^= 1;
+          wc.wait(&sfree[buf], ((sfph >> buf) & 1u) ^ 1u, 7, true);
+          sfph ^= 1u << buf;
           tc_fence_after();
           const uint32_t dS = tbase + buf * 128;
           for (int kc = 0; kc < p.KC; ++kc) {
             wc.wait(&full[stage], ph, 5);
             const unsigned long long t_is = DBG ? clock64() : 0ull;
             tc_fence_after();
-            const uint64_t ad0 = smem_desc_sw128(smem_u32(sA + 2 * kc * kBox), 16, 1024);
-            const uint64_t bd0 = smem_desc_sw128(smem_u32(sStage + stage * kStage), 16, 1024);
+            const int sb = BWD ? 2 : p.sbox;
+            const uint64_t ad0 = smem_desc_sw128(smem_u32(sA + sb * kc * kBox), 16, 1024);
+            const uint64_t bd0 = smem_desc_sw128(smem_u32(sStage + stage * p.stage_bytes), 16, 1024);
             umma_bf16_warp<2>(dS, ad0, bd0, idS, kc != 0);
 #pragma unroll
             for (int k = 1; k < 4; ++k) umma_bf16_warp<2>(dS, ad0 + (uint64_t)(2 * k), bd0 + (uint64_t)(2 * k), idS, 1u);
-            if (2 * kc + 1 < p.KB) {  // odd number of 64-d blocks: the last stage is half used
+            if (sb == 2 && 2 * kc + 1 < p.KB) {  // odd number of 64-d blocks: the last stage is half used
 #pragma unroll
               for (int k = 4; k < 8; ++k)
                 umma_bf16_warp<2>(dS, ad0 + (uint64_t)((kBox >> 4) + 2 * (k & 3)),
@@ -394,7 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int grp = h * 2 + u;     // the 2 warps (rh = 0, 1) that share these 64 columns
     const int et = ep * 32 + lane;  // 0..255
     const uint32_t laddr = tbase + ((uint32_t)(q * 32) << 16) + u * 64;
-    uint32_t sph[kNB] = {}, gfph = 0, daph = 0;
+    uint32_t sph = 0, gfph = 0, daph = 0;  // sph: phase bit of sfull[b] = bit b
     WaitClock<DBG> wc(p.dbg, lane == 0);
     int tile_ctr = 0;
     const float k2 = p.k2;
@@ -405,12 +405,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // backward: this warp's column LSEs for the next tile, prefetched into registers one tile ahead
     // (lane l holds columns 2l, 2l+1 of the warp's 64-column slice) -> no cross-warp barrier per tile
     float2 pc = make_float2(0.f, 0.f);
-    auto load_pc = [&](long long item) {
-      int rbn, ctn;
-      S.decode(item, rbn, ctn);
+    auto load_pc_ct = [&](int ctn) {
       const int j = ctn * kColsPerTile + h * 128 + u * 64 + 2 * lane;
       pc.x = j < p.ncols ? __ldg(p.lse_col2 + j) : 0.f;
       pc.y = j + 1 < p.ncols ? __ldg(p.lse_col2 + j + 1) : 0.f;
+    };
+    auto load_pc = [&](long long item) {
+      int rbn, ctn;
+      S.decode(item, rbn, ctn);
+      load_pc_ct(ctn);
     };
     if (BWD && nk > 0) load_pc(0);
     long long it = 0;
@@ -424,9 +427,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       float mrow[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, srow[4] = {0.f, 0.f, 0.f, 0.f};
       float r2 = 0.f;
       if (BWD && row_ok) r2 = __ldg(p.lse_row2 + ig);
+      const long long seg_start = it;
       for (; it < seg_end; ++it) {
-        int rb_, ct;
-        S.decode(it, rb_, ct);
+        const int ct = ct_first + (int)(it - seg_start);  // a segment's column tiles are consecutive
         const int buf = BWD ? 0 : (tile_ctr & (kNB - 1));
         const int cb = ct * kColsPerTile + h * 128 + u * 64;  // global column of this thread's column 0
         const bool diag_tile = p.diag_on && ig >= cb && ig < cb + 64;
@@ -434,17 +437,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (BWD) {  // publish this tile's column LSEs to the warp's slot, then prefetch the next tile's
           *reinterpret_cast<float2*>(&cval[ep][2 * lane]) = pc;
           __syncwarp();
-          if (it + 1 < nk) load_pc(it + 1);
+          if (it + 1 < seg_end) load_pc_ct(ct + 1);
+          else if (it + 1 < nk) load_pc(it + 1);
         }
-        float2 pre0 = make_float2(-INFINITY, 0.f), pre1 = pre0;  // forward: slot values (prefetch)
+        // forward: the 2 warps of a group each merge 32 of its 64 columns into the slot (prefetched here)
+        float2 pre = make_float2(-INFINITY, 0.f);
         const bool first_visit = it < p.n_ct;
         float2* slot = p.col_slots + (long long)blockIdx.x * p.slot_ld;
-        if (!BWD && rh == 0 && !first_visit) {
-          if (cb + 2 * lane < p.ncols) pre0 = slot[cb + 2 * lane];
-          if (cb + 2 * lane + 1 < p.ncols) pre1 = slot[cb + 2 * lane + 1];
-        }
-        wc.wait(&sfull[buf], sph[buf], 8);
-        sph[buf] ^= 1;
+        const int cm = cb + rh * 32 + lane;  // the column this lane merges
+        if (!BWD && !first_visit && cm < p.ncols) pre = slot[cm];
+        wc.wait(&sfull[buf], (sph >> buf) & 1u, 8);
+        sph ^= 1u << buf;
         tc_fence_after();
         float v[64];
         if constexpr (BWD) {  // 32x32b: thread = one row, 64 consecutive columns
@@ -644,18 +647,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(&sfree[buf], 0);
-          xch[grp][rh][2 * lane] = make_float2(m0, S0);
-          xch[grp][rh][2 * lane + 1] = make_float2(m1, S1);
+          // xch is double-buffered by tile parity: a warp can only rewrite buffer t&1 at tile t+2 after
+          // passing tile t+1's barrier, i.e. after its partner finished reading tile t
+          float2(*xb)[2][64] = xch[tile_ctr & 1];
+          *reinterpret_cast<float4*>(&xb[grp][rh][2 * lane]) = make_float4(m0, S0, m1, S1);
           named_bar_sync(2 + grp, 64);
-          if (rh == 0) {
-            float2 a0 = merge2(xch[grp][0][2 * lane], xch[grp][1][2 * lane]);
-            float2 a1 = merge2(xch[grp][0][2 * lane + 1], xch[grp][1][2 * lane + 1]);
-            if (!first_visit) {
-              a0 = merge2(pre0, a0);
-              a1 = merge2(pre1, a1);
-            }
-            if (cb + 2 * lane < p.ncols) slot[cb + 2 * lane] = a0;
-            if (cb + 2 * lane + 1 < p.ncols) slot[cb + 2 * lane + 1] = a1;
+          {
+            float2 a = merge2(xb[grp][0][rh * 32 + lane], xb[grp][1][rh * 32 + lane]);
+            if (!first_visit) a = merge2(pre, a);
+            if (cm < p.ncols) slot[cm] = a;
           }
         } else {
           // ---------------------------------------------------------- backward: G tile -> smem (bf16)
@@ -769,7 +769,12 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.ncols = a.ncols;
   k.dk = a.dk;
   k.KB = (a.dk + 63) / 64;
-  k.KC = (k.KB + 1) / 2;
+  // forward ring stages hold one 16-KB box (the forward has smem left over after A_R: finer stages keep
+  // more bytes in flight); the backward keeps 32-KB stages (two boxes; its dA stages need them)
+  k.sbox = BWD ? 2 : 1;
+  if (const char* e = getenv("INFCL_SBOX"); e && !BWD) k.sbox = atoi(e) == 2 ? 2 : 1;  // A/B diagnostic
+  k.stage_bytes = k.sbox * kBoxB;
+  k.KC = k.sbox == 2 ? (k.KB + 1) / 2 : k.KB;
   k.NDC = (a.dk + 255) / 256;
   k.n_rb = g.n_rb;
   k.n_ct = g.n_ct;
@@ -805,12 +810,12 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   }
   const long long budget = 232448 - ((static_smem + 1023) / 1024) * 1024;
   const size_t fixed = (size_t)k.KB * kBox + (BWD ? 4 * kBox : 0);
-  int ns = (int)((budget - (long long)fixed) / kStage);
+  int ns = (int)((budget - (long long)fixed) / k.stage_bytes);
   ns = std::min(ns, kMaxStages);
   if (const char* e = getenv("INFCL_STAGES")) ns = std::max(2, std::min(ns, atoi(e)));
   if (ns < 2) return fail(INFCL_ERR_SHAPE, "feature dim too large for the smem budget");
   k.n_stages = ns;
-  const size_t smem = fixed + (size_t)ns * kStage;
+  const size_t smem = fixed + (size_t)ns * k.stage_bytes;
 
   CUtensorMap tmA, tmB;
   infcl_status st = make_tmap_bf16(&tmA, a.A, a.nrows, a.dk, a.ld, 64, 64);
