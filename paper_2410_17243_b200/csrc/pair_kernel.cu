@@ -146,13 +146,23 @@ struct WaitClock {
   // every lane of the role times its waits (a lane-dependent branch here would diverge a converged warp and
   // hide the wait of the lanes that did not time); only lane 0 flushes
   unsigned long long* dbg;
-  bool leader;
+  bool leader, spin;
   unsigned long long acc[ON ? 12 : 1];
-  __device__ WaitClock(unsigned long long* d, bool lead) : dbg(d), leader(lead) {
+  __device__ WaitClock(unsigned long long* d, bool lead, bool sp = false) : dbg(d), leader(lead), spin(sp) {
 #pragma unroll
     for (int i = 0; i < (ON ? 12 : 1); ++i) acc[i] = 0;
   }
   __device__ __forceinline__ void wait(uint64_t* bar, uint32_t par, int tag, bool cluster = false) {
+#ifdef INFCL_PRODUCER_SPIN
+    if (spin) {  // A/B: the single-warp producer roles poll test_wait instead of suspending in try_wait
+      const unsigned long long t0 = ON ? clock64() : 0ull;
+      const uint32_t a = smem_u32(bar);
+      while (!mbar_test_wait(a, par, cluster)) {
+      }
+      if (ON && dbg) acc[tag] += clock64() - t0;
+      return;
+    }
+#endif
     if (!ON || !dbg) {
       if (cluster) mbar_wait_cluster(bar, par, tag);
       else mbar_wait(bar, par, tag);
@@ -227,7 +237,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == kWarpTMA) {
     // ===================================================================== TMA producer (both CTAs)
     if (lane == 0) {
-      WaitClock<DBG> wc(p.dbg, lane == 0);
+      WaitClock<DBG> wc(p.dbg, lane == 0, true);
       int stage = 0;
       uint32_t ph = 0, aph = 0;
       auto load_stage = [&](int c0a, int c1a, int c0b, int c1b) {
@@ -286,7 +296,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================================================================== MMA issuer (leader CTA)
     // the whole warp runs converged (warp-uniform descriptors); elect.sync inside the asm issues
     if (cta == 0) {
-      WaitClock<DBG> wc(p.dbg, lane == 0);
+      WaitClock<DBG> wc(p.dbg, lane == 0, true);
       int stage = 0;
       uint32_t ph = 0, aph = 0, gph = 0, dph = 0;
       uint32_t sfph = 0;  // phase bit of sfree[b] = bit b (a register, not a dynamically indexed array)
@@ -347,15 +357,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int sb = BWD ? 2 : p.sbox;
             const uint64_t ad0 = smem_desc_sw128(smem_u32(sA + sb * kc * kBox), 16, 1024);
             const uint64_t bd0 = smem_desc_sw128(smem_u32(sStage + stage * p.stage_bytes), 16, 1024);
-            umma_bf16_warp<2>(dS, ad0, bd0, idS, kc != 0);
-#pragma unroll
-            for (int k = 1; k < 4; ++k) umma_bf16_warp<2>(dS, ad0 + (uint64_t)(2 * k), bd0 + (uint64_t)(2 * k), idS, 1u);
-            if (sb == 2 && 2 * kc + 1 < p.KB) {  // odd number of 64-d blocks: the last stage is half used
-#pragma unroll
-              for (int k = 4; k < 8; ++k)
-                umma_bf16_warp<2>(dS, ad0 + (uint64_t)((kBox >> 4) + 2 * (k & 3)),
-                                  bd0 + (uint64_t)((kBoxB >> 4) + 2 * (k & 3)), idS, 1u);
-            }
+            if (sb == 2 && 2 * kc + 1 < p.KB)
+              umma_stage_pair<true, (kBox >> 4), (kBoxB >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
+            else  // one box per stage, or the half-used last stage of an odd number of 64-d blocks
+              umma_stage_pair<false, 0, 0>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
             umma_commit_pair_mc_warp(&empty[stage], 0x3);
             if (DBG) wc.acc[11] += clock64() - t_is;
             advance();
@@ -769,10 +774,10 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.ncols = a.ncols;
   k.dk = a.dk;
   k.KB = (a.dk + 63) / 64;
-  // forward ring stages hold one 16-KB box (the forward has smem left over after A_R: finer stages keep
-  // more bytes in flight); the backward keeps 32-KB stages (two boxes; its dA stages need them)
-  k.sbox = BWD ? 2 : 1;
-  if (const char* e = getenv("INFCL_SBOX"); e && !BWD) k.sbox = atoi(e) == 2 ? 2 : 1;  // A/B diagnostic
+  // ring stages hold two 16-KB boxes (8 MMAs per barrier round trip). Measured (DESIGN.md perf log): 16-KB
+  // stages keep more bytes in flight in the forward but are 30 % slower -- the per-stage round trip dominates
+  k.sbox = 2;
+  if (const char* e = getenv("INFCL_SBOX"); e && !BWD) k.sbox = atoi(e) == 1 ? 1 : 2;  // A/B diagnostic
   k.stage_bytes = k.sbox * kBoxB;
   k.KC = k.sbox == 2 ? (k.KB + 1) / 2 : k.KB;
   k.NDC = (a.dk + 255) / 256;

@@ -90,6 +90,27 @@ static __device__ __noinline__ void watchdog_fire(int tag, uint32_t parity) {
          (int)threadIdx.x);
   __trap();
 }
+// non-blocking probe (test_wait never suspends the thread): the spin variants below poll it
+__device__ __forceinline__ bool mbar_test_wait(uint32_t addr, uint32_t parity, bool cluster) {
+  uint32_t ok;
+  if (cluster)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
   uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
@@ -206,6 +227,45 @@ __device__ __forceinline__ void umma_bf16_warp(uint32_t d_tmem, uint64_t a_desc,
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
   }
+}
+// One ring stage of the S GEMM in a single asm block (one elect for all of them): 4 MMAs over a 64-wide K box
+// (descriptors advance by 32 B = 2 in the >>4 start-address field), plus 4 more over the second box of the
+// stage at start offsets +AOFF / +BOFF when TWO_BOX.  The first MMA accumulates iff `accumulate`.  Operands
+// are the low descriptor words of K-major SW128 tiles (start>>4 | LBO field); the high word is the constant
+// SBO = 1024 B | version 1 | SWIZZLE_128B = 0x40004040, so only the low words are moved to uniform registers.
+template <bool TWO_BOX, int AOFF, int BOFF>
+__device__ __forceinline__ void umma_stage_pair(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
+                                                uint32_t accumulate) {
+#define INFCL_MMA2(P) "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, " P ";\n\t"
+#define INFCL_STEP(DA, DB) "add.u32 al, %1, " DA ";\n\tadd.u32 bl, %2, " DB ";\n\tmov.b64 a, {al, hi};\n\tmov.b64 b, {bl, hi};\n\t"
+  if constexpr (TWO_BOX) {
+    asm volatile(
+        "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a, b;\n\t.reg .b32 al, bl, hi;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\tmov.b32 hi, 0x40004040;\n\t"
+        INFCL_STEP("0", "0") INFCL_MMA2("p")
+        INFCL_STEP("2", "2") INFCL_MMA2("t")
+        INFCL_STEP("4", "4") INFCL_MMA2("t")
+        INFCL_STEP("6", "6") INFCL_MMA2("t")
+        INFCL_STEP("%5", "%6") INFCL_MMA2("t")
+        INFCL_STEP("%7", "%8") INFCL_MMA2("t")
+        INFCL_STEP("%9", "%10") INFCL_MMA2("t")
+        INFCL_STEP("%11", "%12") INFCL_MMA2("t")
+        "}" ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate),
+        "n"(AOFF), "n"(BOFF), "n"(AOFF + 2), "n"(BOFF + 2), "n"(AOFF + 4), "n"(BOFF + 4), "n"(AOFF + 6), "n"(BOFF + 6)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a, b;\n\t.reg .b32 al, bl, hi;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\tmov.b32 hi, 0x40004040;\n\t"
+        INFCL_STEP("0", "0") INFCL_MMA2("p")
+        INFCL_STEP("2", "2") INFCL_MMA2("t")
+        INFCL_STEP("4", "4") INFCL_MMA2("t")
+        INFCL_STEP("6", "6") INFCL_MMA2("t")
+        "}" ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+#undef INFCL_STEP
+#undef INFCL_MMA2
 }
 __device__ __forceinline__ void umma_commit_pair_mc_warp(uint64_t* bar, uint16_t mask) {
   asm volatile(
