@@ -146,23 +146,13 @@ struct WaitClock {
   // every lane of the role times its waits (a lane-dependent branch here would diverge a converged warp and
   // hide the wait of the lanes that did not time); only lane 0 flushes
   unsigned long long* dbg;
-  bool leader, spin;
+  bool leader;
   unsigned long long acc[ON ? 12 : 1];
-  __device__ WaitClock(unsigned long long* d, bool lead, bool sp = false) : dbg(d), leader(lead), spin(sp) {
+  __device__ WaitClock(unsigned long long* d, bool lead) : dbg(d), leader(lead) {
 #pragma unroll
     for (int i = 0; i < (ON ? 12 : 1); ++i) acc[i] = 0;
   }
   __device__ __forceinline__ void wait(uint64_t* bar, uint32_t par, int tag, bool cluster = false) {
-#ifdef INFCL_PRODUCER_SPIN
-    if (spin) {  // A/B: the single-warp producer roles poll test_wait instead of suspending in try_wait
-      const unsigned long long t0 = ON ? clock64() : 0ull;
-      const uint32_t a = smem_u32(bar);
-      while (!mbar_test_wait(a, par, cluster)) {
-      }
-      if (ON && dbg) acc[tag] += clock64() - t0;
-      return;
-    }
-#endif
     if (!ON || !dbg) {
       if (cluster) mbar_wait_cluster(bar, par, tag);
       else mbar_wait(bar, par, tag);
@@ -237,7 +227,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == kWarpTMA) {
     // ===================================================================== TMA producer (both CTAs)
     if (lane == 0) {
-      WaitClock<DBG> wc(p.dbg, lane == 0, true);
+      WaitClock<DBG> wc(p.dbg, lane == 0);
       int stage = 0;
       uint32_t ph = 0, aph = 0;
       auto load_stage = [&](int c0a, int c1a, int c0b, int c1b) {
@@ -296,7 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================================================================== MMA issuer (leader CTA)
     // the whole warp runs converged (warp-uniform descriptors); elect.sync inside the asm issues
     if (cta == 0) {
-      WaitClock<DBG> wc(p.dbg, lane == 0, true);
+      WaitClock<DBG> wc(p.dbg, lane == 0);
       int stage = 0;
       uint32_t ph = 0, aph = 0, gph = 0, dph = 0;
       uint32_t sfph = 0;  // phase bit of sfree[b] = bit b (a register, not a dynamically indexed array)

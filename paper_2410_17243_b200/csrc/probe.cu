@@ -346,3 +346,210 @@ extern "C" int infcl_diag_tma_rate(const void* X, int nrows, int d, int mode, in
   probe_tma_kernel<<<nblocks, 64, 6 * 32768 + 1024>>>(a, b, c, mode, iters, nrows, out);
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : -3;
 }
+
+// ------------------------------------------------------------------ S-GEMM loop-structure probe (diagnostic)
+// One CTA pair issues `tiles` S tiles of the forward shape (M=128 pair, N=256, K = 64*KB) through the same
+// umma_stage_pair path as pair_kernel, with optional features switched on by `mode` bits, to find which part
+// of the real loop costs tensor throughput:  1: walk A over KB boxes (else reuse box 0);  2: walk B over
+// `ns` 32-KB stages (else reuse stage 0);  4: rotate 4 TMEM accumulators per tile (else one);  8: commit each
+// stage to a per-stage barrier and wait it `ns` stages later (ring back-pressure without TMA).
+namespace infcl {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    probe_walk_kernel(int tiles, int KB, int ns, int mode, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sA = smem_raw;
+  uint8_t* sB = smem_raw + KB * 8192;
+  __shared__ __align__(8) uint64_t ring[16], done;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x / 32;
+  const uint32_t cta = cluster_ctarank();
+  for (int i = threadIdx.x; i < (KB * 8192 + ns * 32768) / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem_raw)[i] = 0x3c003c00u;
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 16; ++i) mbar_init(&ring[i], 1);
+    mbar_init(&done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<2>(&tmem_base, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  if (cta == 0 && warp == 1) {
+    const uint32_t idS = idesc_bf16(128, 256, 0, 0);
+    const int KC = KB / 2;
+    int stage = 0;
+    uint32_t ph = 0;
+    long long n_stage_total = 0;
+    const long long t0 = clock64();
+    for (int t = 0; t < tiles; ++t) {
+      const uint32_t dS = tbase + ((mode & 4) ? (t & 3) * 128 : 0);
+      for (int kc = 0; kc < KC; ++kc) {
+        if ((mode & 8) && n_stage_total >= ns) {  // the slot's previous use must have completed
+          mbar_wait(&ring[stage], ph ^ 1);
+        }
+        tc_fence_after();
+        const uint32_t a = smem_u32(sA + ((mode & 1) ? 2 * kc * 8192 : 0));
+        const uint32_t b = smem_u32(sB + ((mode & 2) ? stage * 32768 : 0));
+        const uint64_t ad0 = smem_desc_sw128(a, 16, 1024), bd0 = smem_desc_sw128(b, 16, 1024);
+        umma_stage_pair<true, (8192 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
+        if (mode & 8) umma_commit_pair_mc_warp(&ring[stage], 0x1);
+        ++n_stage_total;
+        if (++stage == ns) {
+          stage = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    const long long t1 = clock64();
+    umma_commit_pair_mc_warp(&done, 0x3);
+    mbar_wait(&done, 0);
+    const long long t2 = clock64();
+    if (threadIdx.x == 32) {
+      out[0] = t1 - t0;
+      out[1] = t2 - t0;
+    }
+  }
+  if (cta != 0 && warp == 1) mbar_wait(&done, 0);
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc<2>(tbase, 512);
+}
+}  // namespace infcl
+
+extern "C" int infcl_diag_walk(int tiles, int KB, int ns, int mode, long long* out) {
+  const size_t smem = (size_t)KB * 8192 + (size_t)ns * 32768;
+  if (cudaFuncSetAttribute(infcl::probe_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
+    return -1;
+  infcl::probe_walk_kernel<<<2, 128, smem>>>(tiles, KB, ns, mode, out);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : -3;
+}
+
+// Second loop-structure probe with the real kernel's warp roles (320 threads): warp 9 issues (leader CTA),
+// warp 8 = producer (waits empty[s], arrives full[s]; no TMA), warps 0-7 = epilogue stand-ins (wait sfull[b],
+// tcgen05.ld one 32x32b chunk if mode & 64, arrive sfree[b] on the leader).  mode bits: 16 producer ring,
+// 32 epilogue handshake (4 TMEM buffers).  Grid = 2 * nclusters CTAs.
+namespace infcl {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+    probe_walk2_kernel(int tiles, int KB, int ns, int mode, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sA = smem_raw;
+  uint8_t* sB = smem_raw + KB * 8192;
+  __shared__ __align__(8) uint64_t full[16], empty[16], sfull[4], sfree[4], done;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const uint32_t cta = cluster_ctarank();
+  for (int i = threadIdx.x; i < (KB * 8192 + ns * 32768) / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem_raw)[i] = 0x3c003c00u;
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 16; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&sfull[i], 1);
+      mbar_init(&sfree[i], 16);
+    }
+    mbar_init(&done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 9) tmem_alloc<2>(&tmem_base, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  const int KC = KB / 2;
+  const long long nst = (long long)tiles * KC;
+  if (warp == 9 && cta == 0) {
+    const uint32_t idS = idesc_bf16(128, 256, 0, 0);
+    int stage = 0;
+    uint32_t ph = 0, sfph = 0;
+    long long n = 0;
+    const long long t0 = clock64();
+    for (int t = 0; t < tiles; ++t) {
+      const int buf = t & 3;
+      if (mode & 32) {
+        mbar_wait_cluster(&sfree[buf], ((sfph >> buf) & 1u) ^ 1u);
+        sfph ^= 1u << buf;
+      }
+      tc_fence_after();
+      const uint32_t dS = tbase + buf * 128;
+      for (int kc = 0; kc < KC; ++kc) {
+        if (mode & 16) mbar_wait(&full[stage], ph);
+        else if (n >= ns && !(mode & 128)) mbar_wait(&empty[stage], ph ^ 1);
+        tc_fence_after();
+        const uint64_t ad0 = smem_desc_sw128(smem_u32(sA + 2 * kc * 8192), 16, 1024);
+        const uint64_t bd0 = smem_desc_sw128(smem_u32(sB + stage * 32768), 16, 1024);
+        umma_stage_pair<true, (8192 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
+        if (!(mode & 256)) {
+          umma_commit_pair_mc_warp(&empty[stage], 0x3);
+        } else if (stage & 1) {  // release two stages per commit pair, issued back to back at the odd stage
+          umma_commit_pair_mc_warp(&empty[stage - 1], 0x3);
+          umma_commit_pair_mc_warp(&empty[stage], 0x3);
+        }
+        ++n;
+        if (++stage == ns) {
+          stage = 0;
+          ph ^= 1;
+        }
+      }
+      if (mode & 32) umma_commit_pair_mc_warp(&sfull[buf], 0x3);
+    }
+    const long long t1 = clock64();
+    umma_commit_pair_mc_warp(&done, 0x3);
+    mbar_wait(&done, 0);
+    const long long t2 = clock64();
+    if (lane == 0 && blockIdx.x == 0) {
+      out[0] = t1 - t0;
+      out[1] = t2 - t0;
+    }
+  } else if (warp == 8 && (mode & 16)) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (long long n = 0; n < nst; ++n) {
+        mbar_wait(&empty[stage], ph ^ 1);
+        if (cta == 0) mbar_arrive(&full[stage]);
+        if (++stage == ns) {
+          stage = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp < 8 && (mode & 32)) {
+    uint32_t sph = 0;
+    float sink = 0.f;
+    for (int t = 0; t < tiles; ++t) {
+      const int buf = t & 3;
+      mbar_wait(&sfull[buf], (sph >> buf) & 1u);
+      sph ^= 1u << buf;
+      tc_fence_after();
+      if (mode & 64) {
+        float v[32];
+        tmem_ld32(tbase + ((uint32_t)((warp & 3) * 32) << 16) + buf * 128 + (warp >> 2) * 32, v);
+        tmem_ld_wait();
+        sink += v[lane];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&sfree[buf], 0);
+    }
+    if (sink == 1234.5f) out[3] = 1;
+  }
+  if (!(warp == 9 && cta == 0) && warp == 9) mbar_wait(&done, 0);
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 9) tmem_dealloc<2>(tbase, 512);
+}
+}  // namespace infcl
+
+extern "C" int infcl_diag_walk2(int tiles, int KB, int ns, int mode, int nclusters, long long* out) {
+  const size_t smem = (size_t)KB * 8192 + (size_t)ns * 32768;
+  if (cudaFuncSetAttribute(infcl::probe_walk2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
+    return -1;
+  infcl::probe_walk2_kernel<<<2 * nclusters, 320, smem>>>(tiles, KB, ns, mode, out);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : -3;
+}
