@@ -292,6 +292,59 @@ infcl_status bwd_step(Rank& R, const __nv_bfloat16* rowsA, const float* lse_rows
   return launch_pair_backward(a, st);
 }
 
+// ---- row-chunked single-rank pieces (the host end-to-end entry pipelines PCIe copies against them)
+// forward over stationary rows [r0, r1) of the own block: row partials into rstate, column partials merged
+// into cstate(0) right after the launch (so the slots can be reused by the next chunk)
+infcl_status fwd_chunk(Rank& R, int r0, int r1, float* diag, cudaStream_t st) {
+  PassArgs a{};
+  a.A = R.A + (size_t)r0 * R.L.dk;
+  a.B = R.B;
+  a.nrows = r1 - r0;
+  a.ncols = R.L.bs;
+  a.dk = a.ld = R.L.dk;
+  a.scale = R.s;
+  a.diag_on = 1;
+  a.row_off = r0;
+  a.col_slots = R.slots();
+  a.slot_ld = R.L.slot_ld;
+  a.row_parts = R.rparts();
+  a.diag_out = diag + r0;
+  infcl_status s = launch_pair_forward(a, st);
+  if (s) return s;
+  const PassGeom g = pass_geom(a.nrows, a.ncols);
+  launch_merge_rows(R.rparts(), R.rstate() + r0, a.nrows, g, st);
+  launch_merge_cols(R.slots(), R.L.slot_ld, R.cstate(0), R.L.bs, g, st);
+  return INFCL_OK;
+}
+
+// dT pass over stationary rows [r0, r1) of T (own block of I streamed), then its exact diagonal term
+infcl_status bwd_dT_chunk(Rank& R, int r0, int r1, const float* diag, const float* row_lse, const float* col_lse,
+                          const float* grad, float* dT, cudaStream_t st) {
+  PassArgs a{};
+  a.A = R.B + (size_t)r0 * R.L.dk;
+  a.B = R.A;
+  a.nrows = r1 - r0;
+  a.ncols = R.L.bs;
+  a.dk = a.ld = R.L.dk;
+  a.scale = R.s;
+  a.diag_on = 1;
+  a.row_off = r0;
+  a.lse_row2 = R.own2(1) + r0;
+  a.lse_col2 = R.own2(0);
+  a.dA = dT + (size_t)r0 * R.L.d;
+  a.ld_dA = R.L.d;
+  a.d_out = R.L.dk;
+  a.grad = grad;
+  a.coef_base = (float)((double)R.s / (2.0 * (double)R.b));
+  infcl_status s = launch_pair_backward(a, st);
+  if (s) return s;
+  launch_diag_correction(dT + (size_t)r0 * R.L.d, R.L.d,
+                         static_cast<const __nv_bfloat16*>(R.I_orig) + (size_t)r0 * R.L.d, R.L.d, 0, diag + r0,
+                         row_lse + r0, col_lse + r0, grad, a.coef_base, R.s, a.nrows, R.L.d, st);
+  INFCL_CUDA_TRY(cudaGetLastError());
+  return INFCL_OK;
+}
+
 infcl_status bwd_begin(Rank& R, const float* row_lse, const float* col_lse, float* dI, float* dT, cudaStream_t st) {
   launch_scale_log2(row_lse, R.own2(0), R.L.bs, st);
   launch_scale_log2(col_lse, R.own2(1), R.L.bs, st);
@@ -611,27 +664,85 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
   float* dT = reinterpret_cast<float*>(take((size_t)b * d * 4));
   void* ws = p;
   const size_t wsb = infcl_workspace_bytes(b, d, 1, dt);
-  INFCL_CUDA_TRY(cudaMemcpyAsync(I, I_host, (size_t)b * d * esz, cudaMemcpyHostToDevice, st));
-  INFCL_CUDA_TRY(cudaMemcpyAsync(T, T_host, (size_t)b * d * esz, cudaMemcpyHostToDevice, st));
-  INFCL_CUDA_TRY(cudaMemcpyAsync(lg + 1, &grad_loss, sizeof(float), cudaMemcpyHostToDevice, st));
-  TRY(infcl_forward(nullptr, I, T, dt, b, d, s, 0, 1, r, c, dg, lg, ws, wsb, stream));
-  // the dI device->host copy runs on a side stream while the dT pass computes
-  static cudaStream_t copy_stream = nullptr;
-  static cudaEvent_t ev_dI = nullptr, ev_fwd = nullptr;
-  if (!copy_stream) {
-    INFCL_CUDA_TRY(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
-    INFCL_CUDA_TRY(cudaEventCreateWithFlags(&ev_dI, cudaEventDisableTiming));
-    INFCL_CUDA_TRY(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
+  TRY(validate(I_host, T_host, dt, b, d, s, 0, 1, ws, wsb, wsb));
+  // side streams: host->device copies (cin) and device->host copies (cout) overlap the kernels on `st`
+  static cudaStream_t cin = nullptr, cout = nullptr;
+  static cudaEvent_t evs[24];
+  if (!cin) {
+    INFCL_CUDA_TRY(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+    INFCL_CUDA_TRY(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
+    for (auto& e : evs) INFCL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  INFCL_CUDA_TRY(cudaEventRecord(ev_fwd, st));
-  INFCL_CUDA_TRY(cudaStreamWaitEvent(copy_stream, ev_fwd, 0));
-  INFCL_CUDA_TRY(cudaMemcpyAsync(loss_host, lg, sizeof(float), cudaMemcpyDeviceToHost, copy_stream));
-  TRY(backward_impl(nullptr, I, T, dt, b, d, s, 0, 1, r, c, dg, lg + 1, dI, dT, ws, wsb, stream, ev_dI));
-  INFCL_CUDA_TRY(cudaStreamWaitEvent(copy_stream, ev_dI, 0));
-  INFCL_CUDA_TRY(cudaMemcpyAsync(dI_host, dI, (size_t)b * d * 4, cudaMemcpyDeviceToHost, copy_stream));
-  INFCL_CUDA_TRY(cudaMemcpyAsync(dT_host, dT, (size_t)b * d * 4, cudaMemcpyDeviceToHost, st));
+  const size_t row_bytes = (size_t)d * esz;
+  // bf16: the stationary side is processed in row chunks so that (1) the forward starts on the first chunk of
+  // I while the rest is still in flight and (2) each finished chunk of dT is copied out while the next one
+  // computes (dI is copied out during the whole dT pass).  fp32 inputs run unchunked (their bf16 split needs
+  // the whole block).
+  const int nch = (dt == INFCL_BF16 && b >= 32768) ? 4 : 1;
+  const int64_t chunk = ((b + nch - 1) / nch + 127) / 128 * 128;
+  INFCL_CUDA_TRY(cudaEventRecord(evs[0], st));  // scratch is free once prior work on `st` is done
+  INFCL_CUDA_TRY(cudaStreamWaitEvent(cin, evs[0], 0));
+  INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[0], 0));
+  INFCL_CUDA_TRY(cudaMemcpyAsync(T, T_host, (size_t)b * row_bytes, cudaMemcpyHostToDevice, cin));
+  INFCL_CUDA_TRY(cudaEventRecord(evs[1], cin));
+  for (int k = 0; k < nch; ++k) {
+    const int64_t r0 = std::min<int64_t>(b, k * chunk), r1 = std::min<int64_t>(b, r0 + chunk);
+    if (r1 > r0)
+      INFCL_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(I) + r0 * row_bytes,
+                                     static_cast<const uint8_t*>(I_host) + r0 * row_bytes, (r1 - r0) * row_bytes,
+                                     cudaMemcpyHostToDevice, cin));
+    INFCL_CUDA_TRY(cudaEventRecord(evs[2 + k], cin));
+  }
+  launch_set_scalar(lg + 1, grad_loss, st);
+  if (nch == 1) {
+    INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[2], 0));
+    TRY(infcl_forward(nullptr, I, T, dt, b, d, s, 0, 1, r, c, dg, lg, ws, wsb, stream));
+    INFCL_CUDA_TRY(cudaEventRecord(evs[8], st));
+    INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[8], 0));
+    INFCL_CUDA_TRY(cudaMemcpyAsync(loss_host, lg, sizeof(float), cudaMemcpyDeviceToHost, cout));
+    TRY(backward_impl(nullptr, I, T, dt, b, d, s, 0, 1, r, c, dg, lg + 1, dI, dT, ws, wsb, stream, evs[9]));
+    INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[9], 0));
+    INFCL_CUDA_TRY(cudaMemcpyAsync(dI_host, dI, (size_t)b * d * 4, cudaMemcpyDeviceToHost, cout));
+    INFCL_CUDA_TRY(cudaEventRecord(evs[10], st));
+    INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[10], 0));
+    INFCL_CUDA_TRY(cudaMemcpyAsync(dT_host, dT, (size_t)b * d * 4, cudaMemcpyDeviceToHost, cout));
+  } else {
+    Rank R;
+    TRY(prepare_rank(R, I, T, dt, b, d, s, 1, ws, st));
+    INFCL_CUDA_TRY(cudaMemsetAsync(R.acc(), 0, sizeof(double), st));
+    TRY(fwd_begin(R, st));
+    INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[1], 0));  // all of T
+    for (int k = 0; k < nch; ++k) {
+      const int r0 = (int)std::min<int64_t>(b, k * chunk), r1 = (int)std::min<int64_t>(b, r0 + chunk);
+      INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[2 + k], 0));  // rows [r0, r1) of I
+      if (r1 > r0) TRY(fwd_chunk(R, r0, r1, dg, st));
+    }
+    fwd_finish(R, R.cstate(0), r, c, dg, R.acc(), st);
+    launch_loss_write(R.acc(), lg, b, st);
+    INFCL_CUDA_TRY(cudaEventRecord(evs[8], st));
+    INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[8], 0));
+    INFCL_CUDA_TRY(cudaMemcpyAsync(loss_host, lg, sizeof(float), cudaMemcpyDeviceToHost, cout));
+    // dI pass (whole), then copy dI out while the dT pass runs chunk by chunk
+    TRY(bwd_begin(R, r, c, dI, dT, st));
+    TRY(bwd_step(R, R.A, R.own2(0), R.B, R.own2(1), true, dI, d, lg + 1, st));
+    TRY(pass_end(R, 0, dI, dg, r, c, lg + 1, st));
+    INFCL_CUDA_TRY(cudaEventRecord(evs[9], st));
+    INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[9], 0));
+    INFCL_CUDA_TRY(cudaMemcpyAsync(dI_host, dI, (size_t)b * d * 4, cudaMemcpyDeviceToHost, cout));
+    INFCL_CUDA_TRY(cudaMemsetAsync(dT, 0, (size_t)b * d * 4, st));
+    for (int k = 0; k < nch; ++k) {
+      const int r0 = (int)std::min<int64_t>(b, k * chunk), r1 = (int)std::min<int64_t>(b, r0 + chunk);
+      if (r1 <= r0) continue;
+      TRY(bwd_dT_chunk(R, r0, r1, dg, r, c, lg + 1, dT, st));
+      INFCL_CUDA_TRY(cudaEventRecord(evs[12 + k], st));
+      INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[12 + k], 0));
+      INFCL_CUDA_TRY(cudaMemcpyAsync(dT_host + (size_t)r0 * d, dT + (size_t)r0 * d, (size_t)(r1 - r0) * d * 4,
+                                     cudaMemcpyDeviceToHost, cout));
+    }
+  }
+  INFCL_CUDA_TRY(cudaEventRecord(evs[20], cout));
+  INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[20], 0));  // the call's stream orders after every copy
   INFCL_CUDA_TRY(cudaStreamSynchronize(st));
-  INFCL_CUDA_TRY(cudaStreamSynchronize(copy_stream));
   return INFCL_OK;
 }
 

@@ -109,6 +109,8 @@ __global__ void loss_partial_kernel(const float* __restrict__ r, const float* __
 
 __global__ void loss_write_kernel(const double* acc, float* loss, double inv2b) { *loss = (float)(*acc * inv2b); }
 
+__global__ void set_scalar_kernel(float* dst, float v) { *dst = v; }
+
 __global__ void scale_log2_kernel(const float* __restrict__ x, float* __restrict__ y, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = x[i] * 1.4426950408889634f;
@@ -207,6 +209,10 @@ void launch_loss_partial(const float* r, const float* c, const float* diag, int 
 }
 void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s) {
   loss_write_kernel<<<1, 1, 0, s>>>(acc, loss, 0.5 / (double)b);
+  ++launch_counter();
+}
+void launch_set_scalar(float* dst, float v, cudaStream_t s) {
+  set_scalar_kernel<<<1, 1, 0, s>>>(dst, v);
   ++launch_counter();
 }
 void launch_scale_log2(const float* x, float* y, int n, cudaStream_t s) {

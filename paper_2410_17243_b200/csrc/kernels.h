@@ -20,7 +20,8 @@ struct PassArgs {
   int nrows, ncols;     // valid rows of A and B
   int dk, ld;           // K extent (feature dim) and row stride in elements
   float scale;          // s
-  int diag_on;          // B is A's own block: the positive pair of row i is column i
+  int diag_on;          // B is A's own block: the positive pair of row i is column i + row_off
+  int row_off;          // global index of row 0 (a row chunk of the own block; 0 otherwise)
   // forward outputs (per pass / ring step)
   float2* col_slots;    // [2 * npairs][slot_ld] (m2, sigma) partials (workspace)
   long long slot_ld;
@@ -53,6 +54,7 @@ void launch_finalize_lse(const float2* st, float* lse, float* lse2, int n, cudaS
 void launch_loss_partial(const float* r, const float* c, const float* diag, int n, double* acc, cudaStream_t s);
 void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s);
 void launch_scale_log2(const float* x, float* y, int n, cudaStream_t s);
+void launch_set_scalar(float* dst, float v, cudaStream_t s);
 void launch_diag_correction(float* dA, int ld_dA, const void* B, int ldB, int dtype_f32, const float* diag,
                             const float* r, const float* c, const float* grad, float coef_base, float scale, int n,
                             int d, cudaStream_t s);

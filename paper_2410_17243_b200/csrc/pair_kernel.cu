@@ -61,7 +61,7 @@ struct KParams {
   int sbox, stage_bytes;  // B boxes per ring stage (forward 1 = 16 KB stages, backward 2 = 32 KB) and its bytes
   long long n_items;
   float k2, scale;
-  int diag_on;
+  int diag_on, row_off;
   float2* col_slots;
   long long slot_ld;
   float2* row_parts;
@@ -427,7 +427,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int ct = ct_first + (int)(it - seg_start);  // a segment's column tiles are consecutive
         const int buf = BWD ? 0 : (tile_ctr & (kNB - 1));
         const int cb = ct * kColsPerTile + h * 128 + u * 64;  // global column of this thread's column 0
-        const bool diag_tile = p.diag_on && ig >= cb && ig < cb + 64;
+        const int igd = ig + p.row_off;  // the column holding this row's positive pair
+        const bool diag_tile = p.diag_on && igd >= cb && igd < cb + 64;
         const bool clean = row_ok && (cb + 64 <= p.ncols) && !diag_tile;
         if (BWD) {  // publish this tile's column LSEs to the warp's slot, then prefetch the next tile's
           *reinterpret_cast<float2*>(&cval[ep][2 * lane]) = pc;
@@ -482,11 +483,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           bool rok[4];
 #pragma unroll
           for (int ri = 0; ri < 4; ++ri) rok[ri] = rowbase + 16 * (ri >> 1) + 8 * (ri & 1) < p.nrows;
-          if (p.diag_on && p.diag_out && rowbase < cb + 64 && rowbase + 32 > cb) {  // diagonal tile (rare)
+          if (p.diag_on && p.diag_out && rowbase + p.row_off < cb + 64 && rowbase + p.row_off + 32 > cb) {  // diagonal tile (rare)
 #pragma unroll
             for (int ri = 0; ri < 4; ++ri) {
               const int rg = rowbase + 16 * (ri >> 1) + 8 * (ri & 1);
-              const int o = rg - cb;
+              const int o = rg + p.row_off - cb;
               if (rok[ri] && o >= 0 && o < 64 && ((o >> 1) & 3) == t0) {
                 float dv = 0.f;
 #pragma unroll
@@ -670,8 +671,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 64; j += 2) {
               const int jg = cb + j;
-              const bool ok0 = row_ok && jg < p.ncols && !(p.diag_on && jg == ig);
-              const bool ok1 = row_ok && jg + 1 < p.ncols && !(p.diag_on && jg + 1 == ig);
+              const bool ok0 = row_ok && jg < p.ncols && !(p.diag_on && jg == igd);
+              const bool ok1 = row_ok && jg + 1 < p.ncols && !(p.diag_on && jg + 1 == igd);
               pk[j / 2] &= (ok0 ? 0x0000FFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
             }
           }
@@ -778,6 +779,7 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.k2 = a.scale * 1.4426950408889634f;
   k.scale = a.scale;
   k.diag_on = a.diag_on;
+  k.row_off = a.row_off;
   k.col_slots = a.col_slots;
   k.slot_ld = a.slot_ld;
   k.row_parts = a.row_parts;

@@ -103,3 +103,23 @@ def test_cfg3_codebook_closed_form():
     assert np.abs(c.cpu().numpy() - cf["c"]).max() <= 2e-3
     assert rel_norm(dI.cpu().numpy()[rows], cf["dI"]) <= 2e-3
     assert rel_norm(dT.cpu().numpy()[rows], cf["dT"]) <= 2e-3
+
+
+@pytest.mark.parametrize("b,d", [(32768, 128), (40000, 64)])
+def test_e2e_host_entry_chunked(b, d):
+    """Host end-to-end entry at sizes where it pipelines PCIe copies against row chunks of the forward and of
+    the dT pass (4 chunks; b = 40000 leaves a ragged last chunk): loss and stratified gradient rows against
+    the fp64 oracle (streamed r, c; sampled rows of dI and dT)."""
+    I, T = make_features(b, d, seed=11, dist="paired")
+    loss, dI, dT = K.infcl_loss_grad_host(I.pin_memory(), T.pin_memory(), S)
+    ref = oracle.streamed_forward(I, T, S, chunk=4096)
+    assert abs(loss.item() - ref["loss"]) <= 1e-4 * abs(ref["loss"])
+    rows = stratified_rows(b, 96)
+    # chunk boundaries (the row offset of each chunk's diagonal) are in the sample
+    chunk = ((b + 3) // 4 + 127) // 128 * 128
+    rows = np.unique(np.concatenate([rows, [chunk - 1, chunk, 2 * chunk, 3 * chunk - 1, 3 * chunk]]))
+    rows = rows[rows < b]
+    rdI = oracle.sampled_row_grads(I, T, S, ref["r"], ref["c"], rows)
+    rdT = oracle.sampled_row_grads(T, I, S, ref["c"], ref["r"], rows)
+    assert rel_norm(dI.numpy()[rows], rdI) <= 2e-3
+    assert rel_norm(dT.numpy()[rows], rdT) <= 2e-3
