@@ -435,12 +435,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     probe_walk2_kernel(int tiles, int KB, int ns, int mode, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sA = smem_raw;
-  uint8_t* sB = smem_raw + KB * 8192;
+  const bool wide = (mode & 512) != 0;  // M=256 pair MMAs (128 rows per CTA), 2 TMEM buffers of 256 columns
+  uint8_t* sB = smem_raw + KB * (wide ? 16384 : 8192);
   __shared__ __align__(8) uint64_t full[16], empty[16], sfull[4], sfree[4], done;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const uint32_t cta = cluster_ctarank();
-  for (int i = threadIdx.x; i < (KB * 8192 + ns * 32768) / 4; i += blockDim.x)
+  for (int i = threadIdx.x; i < (KB * (wide ? 16384 : 8192) + ns * 32768) / 4; i += blockDim.x)
     reinterpret_cast<uint32_t*>(smem_raw)[i] = 0x3c003c00u;
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
@@ -463,26 +464,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   const int KC = KB / 2;
   const long long nst = (long long)tiles * KC;
   if (warp == 9 && cta == 0) {
-    const uint32_t idS = idesc_bf16(128, 256, 0, 0);
+    const uint32_t idS = idesc_bf16(wide ? 256 : 128, 256, 0, 0);
     int stage = 0;
     uint32_t ph = 0, sfph = 0;
     long long n = 0;
     const long long t0 = clock64();
     for (int t = 0; t < tiles; ++t) {
-      const int buf = t & 3;
+      const int buf = wide ? (t & 1) : (t & 3);
       if (mode & 32) {
         mbar_wait_cluster(&sfree[buf], ((sfph >> buf) & 1u) ^ 1u);
         sfph ^= 1u << buf;
       }
       tc_fence_after();
-      const uint32_t dS = tbase + buf * 128;
+      const uint32_t dS = tbase + buf * (wide ? 256 : 128);
       for (int kc = 0; kc < KC; ++kc) {
         if (mode & 16) mbar_wait(&full[stage], ph);
         else if (n >= ns && !(mode & 128)) mbar_wait(&empty[stage], ph ^ 1);
         tc_fence_after();
-        const uint64_t ad0 = smem_desc_sw128(smem_u32(sA + 2 * kc * 8192), 16, 1024);
+        const uint64_t ad0 = smem_desc_sw128(smem_u32(sA + 2 * kc * (wide ? 16384 : 8192)), 16, 1024);
         const uint64_t bd0 = smem_desc_sw128(smem_u32(sB + stage * 32768), 16, 1024);
-        umma_stage_pair<true, (8192 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
+        if (wide) umma_stage_pair<true, (16384 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
+        else umma_stage_pair<true, (8192 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
         if (!(mode & 256)) {
           umma_commit_pair_mc_warp(&empty[stage], 0x3);
         } else if (stage & 1) {  // release two stages per commit pair, issued back to back at the odd stage
@@ -522,13 +524,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     uint32_t sph = 0;
     float sink = 0.f;
     for (int t = 0; t < tiles; ++t) {
-      const int buf = t & 3;
+      const int buf = wide ? (t & 1) : (t & 3);
       mbar_wait(&sfull[buf], (sph >> buf) & 1u);
       sph ^= 1u << buf;
       tc_fence_after();
       if (mode & 64) {
         float v[32];
-        tmem_ld32(tbase + ((uint32_t)((warp & 3) * 32) << 16) + buf * 128 + (warp >> 2) * 32, v);
+        tmem_ld32(tbase + ((uint32_t)((warp & 3) * 32) << 16) + buf * (wide ? 256 : 128) + (warp >> 2) * 32, v);
         tmem_ld_wait();
         sink += v[lane];
       }
@@ -547,7 +549,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
 }  // namespace infcl
 
 extern "C" int infcl_diag_walk2(int tiles, int KB, int ns, int mode, int nclusters, long long* out) {
-  const size_t smem = (size_t)KB * 8192 + (size_t)ns * 32768;
+  const size_t smem = (size_t)KB * ((mode & 512) ? 16384 : 8192) + (size_t)ns * 32768;
   if (cudaFuncSetAttribute(infcl::probe_walk2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
     return -1;
   infcl::probe_walk2_kernel<<<2 * nclusters, 320, smem>>>(tiles, KB, ns, mode, out);
