@@ -27,6 +27,7 @@
 
 #include "host_utils.h"
 #include "kernels.h"
+#include "pair_common.cuh"
 #include "ptx.cuh"
 
 namespace infcl {
@@ -48,127 +49,6 @@ static void prof_clear() {
     }
   for (auto& v : prof().ev) v.clear();
 }
-
-constexpr int kThreads = 320;  // warps 0-7 epilogue, warp 8 TMA, warp 9 MMA
-constexpr int kWarpTMA = 8, kWarpMMA = 9;
-constexpr int kBox = 8192;     // A_R / G block: 64 rows x 64 bf16 (128 B, SW128)
-constexpr int kBoxB = 16384;   // streamed B box: 128 rows x 64 bf16 (128 B, SW128)
-constexpr int kMaxStages = 16;
-
-struct KParams {
-  int nrows, ncols, dk, KB, KC, NDC;
-  int n_rb, n_ct, npairs, n_stages;
-  int sbox, stage_bytes;  // B boxes per ring stage (forward 1 = 16 KB stages, backward 2 = 32 KB) and its bytes
-  long long n_items;
-  float k2, scale;
-  int diag_on, row_off;
-  float2* col_slots;
-  long long slot_ld;
-  float2* row_parts;
-  float* diag_out;
-  const float* lse_row2;
-  const float* lse_col2;
-  float* dA;
-  int ld_dA, d_out;
-  const float* grad;
-  float coef_base;
-  unsigned long long* dbg;  // optional per-tag wait-cycle accumulators (INFCL_DEBUG_WAITS)
-  int noepi;                // diagnostic: epilogue skips its math (results invalid; INFCL_DEBUG_NOEPI)
-  int notma;                // diagnostic: producer signals stages without loading (results invalid)
-};
-
-// Column-synchronous schedule.  Full waves: pair p owns row block w*P + p for w < W = n_rb / P and sweeps all
-// column tiles in order, so all pairs stream the same B tiles at about the same time (each tile is read from
-// HBM once and served from L2 to the other pairs).  Tail: the remaining R = n_rb - W*P row blocks x n_ct tiles
-// are split into P contiguous ranges (row-major), so the last wave stays balanced.  Segment = consecutive
-// items of one row block; row-partial slot of a segment: rb (full waves) or n_rb + p + (rb - W*P) (tail).
-struct Sched {
-  int P, W, n_ct, n_rb, pair;
-  long long tb, te;  // this pair's tail range (tail item indices)
-  __device__ Sched(int n_rb_, int n_ct_, int P_, int pair_) : P(P_), n_ct(n_ct_), n_rb(n_rb_), pair(pair_) {
-    W = n_rb / P;
-    const long long T = (long long)(n_rb - W * P) * n_ct;
-    tb = (long long)pair * T / P;
-    te = (long long)(pair + 1) * T / P;
-  }
-  __device__ long long n_local() const { return (long long)W * n_ct + (te - tb); }
-  __device__ void decode(long long k, int& rb, int& ct) const {
-    const long long kw = (long long)W * n_ct;
-    if (k < kw) {
-      rb = (int)(k / n_ct) * P + pair;
-      ct = (int)(k % n_ct);
-    } else {
-      const long long t = tb + (k - kw);
-      rb = W * P + (int)(t / n_ct);
-      ct = (int)(t % n_ct);
-    }
-  }
-  __device__ long long seg_end(long long k) const {  // exclusive local index where k's segment ends
-    const long long kw = (long long)W * n_ct;
-    if (k < kw) return (k / n_ct + 1) * n_ct;
-    const long long t = tb + (k - kw);
-    return kw + std::min<long long>(te, (t / n_ct + 1) * n_ct) - tb;
-  }
-  __device__ long long seg_slot(int rb) const { return rb < W * P ? rb : (long long)n_rb + pair + (rb - W * P); }
-};
-
-__device__ __forceinline__ float2 merge2(float2 a, float2 b) {
-  const float M = fmaxf(a.x, b.x);
-  if (M == -INFINITY) return make_float2(-INFINITY, 0.f);
-  return make_float2(M, a.y * ex2(a.x - M) + b.y * ex2(b.x - M));
-}
-
-// Transposed butterfly reduction of 32 values per lane: afterwards lane l holds op over the 32 lanes of
-// the value originally at index l (5 rounds, 31 shuffles).
-template <bool IS_MAX>
-__device__ __forceinline__ float xreduce32(float (&t)[32], int lane) {
-#define XR_ROUND(O, N)                                                 \
-  {                                                                    \
-    const bool up = (lane & (O)) != 0;                                 \
-    _Pragma("unroll") for (int i = 0; i < (N); ++i) {                  \
-      const float send = up ? t[i] : t[i + (N)];                       \
-      const float keep = up ? t[i + (N)] : t[i];                       \
-      const float recv = __shfl_xor_sync(0xffffffffu, send, (O));      \
-      t[i] = IS_MAX ? fmaxf(keep, recv) : keep + recv;                 \
-    }                                                                  \
-  }
-  XR_ROUND(16, 16)
-  XR_ROUND(8, 8)
-  XR_ROUND(4, 4)
-  XR_ROUND(2, 2)
-  XR_ROUND(1, 1)
-#undef XR_ROUND
-  return t[0];
-}
-
-template <bool ON>
-struct WaitClock {
-  // every lane of the role times its waits (a lane-dependent branch here would diverge a converged warp and
-  // hide the wait of the lanes that did not time); only lane 0 flushes
-  unsigned long long* dbg;
-  bool leader;
-  unsigned long long acc[ON ? 12 : 1];
-  __device__ WaitClock(unsigned long long* d, bool lead) : dbg(d), leader(lead) {
-#pragma unroll
-    for (int i = 0; i < (ON ? 12 : 1); ++i) acc[i] = 0;
-  }
-  __device__ __forceinline__ void wait(uint64_t* bar, uint32_t par, int tag, bool cluster = false) {
-    if (!ON || !dbg) {
-      if (cluster) mbar_wait_cluster(bar, par, tag);
-      else mbar_wait(bar, par, tag);
-      return;
-    }
-    const unsigned long long t0 = clock64();
-    if (cluster) mbar_wait_cluster(bar, par, tag);
-    else mbar_wait(bar, par, tag);
-    acc[tag] += clock64() - t0;
-  }
-  __device__ void flush(int role) {
-    if (!ON || !dbg || !leader) return;
-    for (int i = 0; i < 12; ++i)
-      if (acc[i]) atomicAdd(dbg + role * 16 + i, acc[i]);
-  }
-};
 
 template <bool BWD, bool DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -402,8 +282,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     float2 pc = make_float2(0.f, 0.f);
     auto load_pc_ct = [&](int ctn) {
       const int j = ctn * kColsPerTile + h * 128 + u * 64 + 2 * lane;
-      pc.x = j < p.ncols ? __ldg(p.lse_col2 + j) : 0.f;
-      pc.y = j + 1 < p.ncols ? __ldg(p.lse_col2 + j + 1) : 0.f;
+      pc.x = j < p.ncols ? __ldg(p.lse_col2 + j) : INFINITY;  // +inf: no column (G masked; excluded from cmin)
+      pc.y = j + 1 < p.ncols ? __ldg(p.lse_col2 + j + 1) : INFINITY;
     };
     auto load_pc = [&](long long item) {
       int rbn, ctn;
@@ -420,8 +300,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const bool row_ok = ig < p.nrows;
       // forward (16x256b layout): running (m, sigma) of this thread's 4 rows over its 16-column slice
       float mrow[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, srow[4] = {0.f, 0.f, 0.f, 0.f};
-      float r2 = 0.f;
-      if (BWD && row_ok) r2 = __ldg(p.lse_row2 + ig);
+      float r2 = 0.f, rmax = -INFINITY;  // backward: row LSE (log2) and its maximum over the warp's valid rows
+      if (BWD) {
+        if (row_ok) r2 = __ldg(p.lse_row2 + ig);
+        rmax = row_ok ? r2 : -INFINITY;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+      }
       const long long seg_start = it;
       for (; it < seg_end; ++it) {
         const int ct = ct_first + (int)(it - seg_start);  // a segment's column tiles are consecutive
@@ -430,8 +315,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int igd = ig + p.row_off;  // the column holding this row's positive pair
         const bool diag_tile = p.diag_on && igd >= cb && igd < cb + 64;
         const bool clean = row_ok && (cb + 64 <= p.ncols) && !diag_tile;
-        if (BWD) {  // publish this tile's column LSEs to the warp's slot, then prefetch the next tile's
-          *reinterpret_cast<float2*>(&cval[ep][2 * lane]) = pc;
+        // backward: G_ij = 2^{y-r2_i} + 2^{y-c2_j} = E (1 + p_i q_j) with E = 2^{y-r2_i}, p_i = 2^{r2_i-cmin},
+        // q_j = 2^{cmin-c2_j} (cmin = the tile's smallest column LSE of this warp): one exponential per logit.
+        // Valid while every r2_i - c2_j <= 60 (then a lost underflowed E carries a term < 2^-66); otherwise
+        // (warp-uniform, rare) the tile takes both exponentials.  cval holds q (fast) or c2 (exact).
+        float cmin = INFINITY;
+        bool gfast = true;
+        if (BWD) {  // publish this tile's column terms to the warp's slot, then prefetch the next tile's
+          cmin = fminf(pc.x, pc.y);
+#pragma unroll
+          for (int o = 16; o; o >>= 1) cmin = fminf(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+          gfast = !(rmax - cmin > 60.f);
+          const float2 cq = gfast ? make_float2(ex2(cmin - pc.x), ex2(cmin - pc.y)) : pc;
+          *reinterpret_cast<float2*>(&cval[ep][2 * lane]) = cq;
           __syncwarp();
           if (it + 1 < seg_end) load_pc_ct(ct + 1);
           else if (it + 1 < nk) load_pc(it + 1);
@@ -478,167 +374,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           //   row  32*rh + 16*eta + 8*kap + t1 (of this CTA's 64),  column cb + 8*rho + 2*t0 + c.
           // Row references are thread-local maxima (any upper bound works for shared exponentials), so rows
           // need no shuffles; column sums reduce 4 rows in-thread, then 8 lanes (3 butterfly rounds).
-          const int t0 = lane & 3, t1 = lane >> 2;
-          const int rowbase = rb * kRowsPerPair + (int)cta * 64 + rh * 32 + t1;
-          bool rok[4];
-#pragma unroll
-          for (int ri = 0; ri < 4; ++ri) rok[ri] = rowbase + 16 * (ri >> 1) + 8 * (ri & 1) < p.nrows;
-          if (p.diag_on && p.diag_out && rowbase + p.row_off < cb + 64 && rowbase + p.row_off + 32 > cb) {  // diagonal tile (rare)
-#pragma unroll
-            for (int ri = 0; ri < 4; ++ri) {
-              const int rg = rowbase + 16 * (ri >> 1) + 8 * (ri & 1);
-              const int o = rg + p.row_off - cb;
-              if (rok[ri] && o >= 0 && o < 64 && ((o >> 1) & 3) == t0) {
-                float dv = 0.f;
-#pragma unroll
-                for (int rho = 0; rho < 8; ++rho)
-#pragma unroll
-                  for (int c = 0; c < 2; ++c)
-                    dv = (8 * rho + 2 * t0 + c == o) ? v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + c] : dv;
-                p.diag_out[rg] = dv * p.scale;
-              }
-            }
-          }
-          const bool ragged = !(rok[0] && rok[1] && rok[2] && rok[3]) || cb + 64 > p.ncols;
-          if (ragged) {
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-              const int ri = (i >> 5) * 2 + ((i >> 1) & 1);
-              const int col = cb + 8 * ((i >> 2) & 7) + 2 * t0 + (i & 1);
-              v[i] = (rok[ri] && col < p.ncols) ? v[i] : -INFINITY;
-            }
-          }
-          float ml[4];  // per-row local maxima (log2 units)
-#pragma unroll
-          for (int ri = 0; ri < 4; ++ri) {
-            float mv = -INFINITY;
-#pragma unroll
-            for (int rho = 0; rho < 8; ++rho)
-#pragma unroll
-              for (int c = 0; c < 2; ++c) mv = fmaxf(mv, v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + c]);
-            ml[ri] = mv == -INFINITY ? -INFINITY : mv * k2;
-          }
-          // shared exponentials E = 2^{y - ml} (y = v * s * log2 e), row sums. Branch-free so the 4 rows'
-          // exponentials interleave: an all-masked row uses reference 0 and its -inf logits give E = 0.
-#pragma unroll
-          for (int ri = 0; ri < 4; ++ri) {
-            const float ref = ml[ri] == -INFINITY ? 0.f : ml[ri];
-            float part[8];
-#pragma unroll
-            for (int rho = 0; rho < 8; ++rho) {
-              float& x0 = v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2];
-              float& x1 = v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + 1];
-              x0 = ex2(fmaf(x0, k2, -ref));
-              x1 = ex2(fmaf(x1, k2, -ref));
-              part[rho] = x0 + x1;
-            }
-            const float acc = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
-            const float mn = fmaxf(mrow[ri], ml[ri]);
-            const float a_old = mrow[ri] == -INFINITY ? 0.f : ex2(mrow[ri] - mn);
-            const float a_new = ml[ri] == -INFINITY ? 0.f : ex2(ml[ri] - mn);
-            srow[ri] = srow[ri] * a_old + acc * a_new;
-            mrow[ri] = mn;
-          }
-          float Rw = fmaxf(fmaxf(ml[0], ml[1]), fmaxf(ml[2], ml[3]));
-#pragma unroll
-          for (int o = 16; o; o >>= 1) Rw = fmaxf(Rw, __shfl_xor_sync(0xffffffffu, Rw, o));
-          float w[4];
-#pragma unroll
-          for (int ri = 0; ri < 4; ++ri) w[ri] = ml[ri] == -INFINITY ? 0.f : ex2(ml[ri] - Rw);
-          float P[16];  // column partials over this thread's 4 rows: index rho*2 + c
-#pragma unroll
-          for (int rho = 0; rho < 8; ++rho)
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              float a = v[rho * 4 + c] * w[0];
-              a = fmaf(v[rho * 4 + 2 + c], w[1], a);
-              a = fmaf(v[32 + rho * 4 + c], w[2], a);
-              a = fmaf(v[32 + rho * 4 + 2 + c], w[3], a);
-              P[rho * 2 + c] = a;
-            }
-          // transposed butterfly over lane bits 4,3,2 -> lane holds columns 2*lane, 2*lane+1
-#define XR16(O, N)                                                     \
-  {                                                                    \
-    const bool up = (lane & (O)) != 0;                                 \
-    _Pragma("unroll") for (int i = 0; i < (N); ++i) {                  \
-      const float send = up ? P[i] : P[i + (N)];                       \
-      const float keep = up ? P[i + (N)] : P[i];                       \
-      P[i] = keep + __shfl_xor_sync(0xffffffffu, send, (O));           \
-    }                                                                  \
-  }
-          XR16(16, 8)
-          XR16(8, 4)
-          XR16(4, 2)
-#undef XR16
-          float S0 = P[0], S1 = P[1];
-          float m0 = Rw, m1 = Rw;
-          const bool bad = Rw != -INFINITY && ((cb + 2 * lane < p.ncols && S0 < 8.6736174e-19f) ||
-                                               (cb + 2 * lane + 1 < p.ncols && S1 < 8.6736174e-19f));  // < 2^-60
-          if (__any_sync(0xffffffffu, bad)) {
-            // exact fallback (rare: a column far below the tile maximum): exact column max, second exponential
-            float y[64];
-            tmem_ld16x256x8(laddr + buf * 128, y);
-            tmem_ld16x256x8(laddr + (16u << 16) + buf * 128, y + 32);
-            tmem_ld_wait();
-            float cm[16];
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-              const int ri = (i >> 5) * 2 + ((i >> 1) & 1);
-              const int col = cb + 8 * ((i >> 2) & 7) + 2 * t0 + (i & 1);
-              y[i] = (rok[ri] && col < p.ncols) ? y[i] * k2 : -INFINITY;
-            }
-#pragma unroll
-            for (int rho = 0; rho < 8; ++rho)
-#pragma unroll
-              for (int c = 0; c < 2; ++c)
-                cm[rho * 2 + c] = fmaxf(fmaxf(y[rho * 4 + c], y[rho * 4 + 2 + c]),
-                                        fmaxf(y[32 + rho * 4 + c], y[32 + rho * 4 + 2 + c]));
-#define XM16(O, N)                                                     \
-  {                                                                    \
-    const bool up = (lane & (O)) != 0;                                 \
-    _Pragma("unroll") for (int i = 0; i < (N); ++i) {                  \
-      const float send = up ? cm[i] : cm[i + (N)];                     \
-      const float keep = up ? cm[i + (N)] : cm[i];                     \
-      cm[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, (O)));    \
-    }                                                                  \
-  }
-            XM16(16, 8)
-            XM16(8, 4)
-            XM16(4, 2)
-#undef XM16
-            m0 = cm[0];
-            m1 = cm[1];
-#pragma unroll
-            for (int rho = 0; rho < 8; ++rho) {
-              const float c0 = __shfl_sync(0xffffffffu, m0, 4 * rho + t0);  // max of column 8rho+2t0
-              const float c1 = __shfl_sync(0xffffffffu, m1, 4 * rho + t0);  // max of column 8rho+2t0+1
-#pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                const float cc = c ? c1 : c0;
-                float a = 0.f;
-                if (cc != -INFINITY) {
-                  a = ex2(y[rho * 4 + c] - cc) + ex2(y[rho * 4 + 2 + c] - cc) + ex2(y[32 + rho * 4 + c] - cc) +
-                      ex2(y[32 + rho * 4 + 2 + c] - cc);
-                }
-                P[rho * 2 + c] = a;
-              }
-            }
-#define XR16(O, N)                                                     \
-  {                                                                    \
-    const bool up = (lane & (O)) != 0;                                 \
-    _Pragma("unroll") for (int i = 0; i < (N); ++i) {                  \
-      const float send = up ? P[i] : P[i + (N)];                       \
-      const float keep = up ? P[i + (N)] : P[i];                       \
-      P[i] = keep + __shfl_xor_sync(0xffffffffu, send, (O));           \
-    }                                                                  \
-  }
-            XR16(16, 8)
-            XR16(8, 4)
-            XR16(4, 2)
-#undef XR16
-            S0 = P[0];
-            S1 = P[1];
-          }
+          const int rowbase = rb * kRowsPerPair + (int)cta * 64 + rh * 32 + (lane >> 2);
+          const float4 cs = fwd_chunk_stats(v, laddr + buf * 128, rowbase, cb, p, lane, mrow, srow);
+          const float m0 = cs.x, S0 = cs.y, m1 = cs.z, S1 = cs.w;
           // release this S buffer (per warp) only after the (rare) exact fallback has re-read it
           tc_fence_before();
           __syncwarp();
@@ -657,15 +395,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           // ---------------------------------------------------------- backward: G tile -> smem (bf16)
           const float* cv = cval[ep];
           uint32_t pk[32];
+          if (gfast) {
+            const float pr = ex2(r2 - cmin);
+            const float2 kk = make_float2(k2, k2), nr = make_float2(-r2, -r2), pp = make_float2(pr, pr);
 #pragma unroll
-          for (int j = 0; j < 64; j += 4) {
-            const float4 c4 = *reinterpret_cast<const float4*>(cv + j);
-            const float g0 = ex2(fmaf(v[j + 0], k2, -r2)) + ex2(fmaf(v[j + 0], k2, -c4.x));
-            const float g1 = ex2(fmaf(v[j + 1], k2, -r2)) + ex2(fmaf(v[j + 1], k2, -c4.y));
-            const float g2 = ex2(fmaf(v[j + 2], k2, -r2)) + ex2(fmaf(v[j + 2], k2, -c4.z));
-            const float g3 = ex2(fmaf(v[j + 3], k2, -r2)) + ex2(fmaf(v[j + 3], k2, -c4.w));
-            pk[j / 2] = pack_bf16(g0, g1);
-            pk[j / 2 + 1] = pack_bf16(g2, g3);
+            for (int j = 0; j < 64; j += 4) {
+              const float4 q4 = *reinterpret_cast<const float4*>(cv + j);
+              const float2 t0 = __ffma2_rn(make_float2(v[j + 0], v[j + 1]), kk, nr);
+              const float2 t1 = __ffma2_rn(make_float2(v[j + 2], v[j + 3]), kk, nr);
+              const float2 e0 = make_float2(ex2(t0.x), ex2(t0.y)), e1 = make_float2(ex2(t1.x), ex2(t1.y));
+              const float2 g0 = __ffma2_rn(e0, __fmul2_rn(pp, make_float2(q4.x, q4.y)), e0);
+              const float2 g1 = __ffma2_rn(e1, __fmul2_rn(pp, make_float2(q4.z, q4.w)), e1);
+              pk[j / 2] = pack_bf16(g0.x, g0.y);
+              pk[j / 2 + 1] = pack_bf16(g1.x, g1.y);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 64; j += 4) {
+              const float4 c4 = *reinterpret_cast<const float4*>(cv + j);
+              const float g0 = ex2(fmaf(v[j + 0], k2, -r2)) + ex2(fmaf(v[j + 0], k2, -c4.x));
+              const float g1 = ex2(fmaf(v[j + 1], k2, -r2)) + ex2(fmaf(v[j + 1], k2, -c4.y));
+              const float g2 = ex2(fmaf(v[j + 2], k2, -r2)) + ex2(fmaf(v[j + 2], k2, -c4.z));
+              const float g3 = ex2(fmaf(v[j + 3], k2, -r2)) + ex2(fmaf(v[j + 3], k2, -c4.w));
+              pk[j / 2] = pack_bf16(g0, g1);
+              pk[j / 2 + 1] = pack_bf16(g2, g3);
+            }
           }
           if (!clean) {  // ragged columns, invalid row, or the diagonal (added exactly in fp32 later)
 #pragma unroll

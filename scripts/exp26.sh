@@ -1,0 +1,3 @@
+#!/bin/bash
+python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
+VARS="prev new" REPS=9 bash scripts/ab.sh
