@@ -11,6 +11,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -151,7 +152,10 @@ Layout make_layout(int64_t b, int d, int world, infcl_dtype dt) {
     return at;
   };
   L.off_slots = take((size_t)2 * L.g.npairs * L.slot_ld * sizeof(float2));
-  L.off_rparts = take((size_t)(L.g.n_rb + 2 * L.g.npairs) * kRowsPerPair * sizeof(float2));
+  // row partials: (row blocks + 2 x pairs) x rows-per-pair slots of whichever kernel runs (narrow or wide)
+  const PassGeom gw = wide_geom(L.bs, L.bs);
+  L.off_rparts = take(std::max((size_t)(L.g.n_rb + 2 * L.g.npairs) * L.g.rpp,
+                               (size_t)(gw.n_rb + 2 * gw.npairs) * gw.rpp) * sizeof(float2));
   L.off_rstate = take((size_t)L.bs * sizeof(float2));
   L.off_cstate = take((size_t)3 * L.bs * sizeof(float2));
   L.off_own2 = take((size_t)2 * L.bs * sizeof(float));
@@ -257,12 +261,12 @@ infcl_status fwd_step_main(Rank& R, const __nv_bfloat16* held, bool own, float* 
   a.diag_out = own ? diag : nullptr;
   infcl_status s = launch_pair_forward(a, st);
   if (s) return s;
-  launch_merge_rows(R.rparts(), R.rstate(), R.L.bs, R.L.g, st);
+  launch_merge_rows(R.rparts(), R.rstate(), R.L.bs, fwd_geom(R.L.bs, R.L.bs), st);
   return INFCL_OK;
 }
 
 void fwd_step_cols(Rank& R, float2* held_cstate, cudaStream_t st) {
-  launch_merge_cols(R.slots(), R.L.slot_ld, held_cstate, R.L.bs, R.L.g, st);
+  launch_merge_cols(R.slots(), R.L.slot_ld, held_cstate, R.L.bs, fwd_geom(R.L.bs, R.L.bs), st);
 }
 
 void fwd_finish(Rank& R, const float2* own_cstate, float* row_lse, float* col_lse, const float* diag, double* acc,
@@ -311,7 +315,7 @@ infcl_status fwd_chunk(Rank& R, int r0, int r1, float* diag, cudaStream_t st) {
   a.diag_out = diag + r0;
   infcl_status s = launch_pair_forward(a, st);
   if (s) return s;
-  const PassGeom g = pass_geom(a.nrows, a.ncols);
+  const PassGeom g = fwd_geom(a.nrows, a.ncols);
   launch_merge_rows(R.rparts(), R.rstate() + r0, a.nrows, g, st);
   launch_merge_cols(R.slots(), R.L.slot_ld, R.cstate(0), R.L.bs, g, st);
   return INFCL_OK;

@@ -41,20 +41,20 @@ __global__ void init_state_kernel(float2* st, int n) {
 }
 
 __global__ void merge_rows_kernel(const float2* __restrict__ parts, float2* __restrict__ state, int nrows, int n_rb,
-                                  int n_ct, int P) {
+                                  int n_ct, int P, int rpp) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
-  const int rb = i / kRowsPerPair;
+  const int rb = i / rpp;
   const int W = n_rb / P;
   float2 acc = state[i];
   if (rb < W * P) {
-    acc = merge_ms(acc, parts[(long long)rb * kRowsPerPair + (i % kRowsPerPair)]);
+    acc = merge_ms(acc, parts[(long long)rb * rpp + (i % rpp)]);
   } else {
     const long long T = (long long)(n_rb - W * P) * n_ct;
     const long long t0 = (long long)(rb - W * P) * n_ct;
     const int p0 = tail_pair_of(t0, T, P), p1 = tail_pair_of(t0 + n_ct - 1, T, P);
     for (int p = p0; p <= p1; ++p)
-      acc = merge_ms(acc, parts[((long long)n_rb + p + (rb - W * P)) * kRowsPerPair + (i % kRowsPerPair)]);
+      acc = merge_ms(acc, parts[((long long)n_rb + p + (rb - W * P)) * rpp + (i % rpp)]);
   }
   state[i] = acc;
 }
@@ -191,7 +191,7 @@ void launch_init_state(float2* st, int n, cudaStream_t s) {
   ++launch_counter();
 }
 void launch_merge_rows(const float2* parts, float2* state, int nrows, const PassGeom& g, cudaStream_t s) {
-  merge_rows_kernel<<<nblk(nrows, 256), 256, 0, s>>>(parts, state, nrows, g.n_rb, g.n_ct, g.npairs);
+  merge_rows_kernel<<<nblk(nrows, 256), 256, 0, s>>>(parts, state, nrows, g.n_rb, g.n_ct, g.npairs, g.rpp);
   ++launch_counter();
 }
 void launch_merge_cols(const float2* slots, long long slot_ld, float2* state, int ncols, const PassGeom& g,

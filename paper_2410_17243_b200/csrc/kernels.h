@@ -39,11 +39,21 @@ struct PassArgs {
 struct PassGeom {
   int n_rb, n_ct, npairs;
   long long n_items;
+  int rpp;  // stationary rows per CTA pair: 128 (narrow pair kernel) or 256 (wide forward kernel)
 };
 
-PassGeom pass_geom(int nrows, int ncols);
-infcl_status launch_pair_forward(const PassArgs& a, cudaStream_t s);
+PassGeom pass_geom(int nrows, int ncols);  // narrow pair kernel (backward; forward with INFCL_FWD_NARROW)
+PassGeom wide_geom(int nrows, int ncols);  // wide forward kernel
+PassGeom fwd_geom(int nrows, int ncols);   // geometry of the forward kernel launch_pair_forward uses
+bool wide_forward_enabled();
+infcl_status launch_pair_forward(const PassArgs& a, cudaStream_t s);  // wide forward unless INFCL_FWD_NARROW
+infcl_status launch_wide_forward(const PassArgs& a, cudaStream_t s);
 infcl_status launch_pair_backward(const PassArgs& a, cudaStream_t s);
+// launch bookkeeping shared by the pair kernels (pair_kernel.cu)
+cudaEvent_t profile_begin(cudaStream_t s);
+void profile_end(int kind, cudaEvent_t e0, cudaStream_t s);
+unsigned long long* debug_buffer(cudaStream_t s);  // INFCL_DEBUG_WAITS accumulators (zeroed) or nullptr
+void debug_report(const char* name, int npairs, cudaStream_t s);
 
 // auxiliary kernels (aux_kernels.cu)
 void launch_init_state(float2* st, int n, cudaStream_t s);

@@ -501,6 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------------------------------ host side
 PassGeom pass_geom(int nrows, int ncols) {
   PassGeom g;
+  g.rpp = kRowsPerPair;
   g.n_rb = (nrows + kRowsPerPair - 1) / kRowsPerPair;
   g.n_ct = (ncols + kColsPerTile - 1) / kColsPerTile;
   g.n_items = (long long)g.n_rb * g.n_ct;
@@ -545,13 +546,9 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.d_out = a.d_out;
   k.grad = a.grad;
   k.coef_base = a.coef_base;
-  static unsigned long long* dbg_buf = nullptr;
-  static const bool dbg_on = getenv("INFCL_DEBUG_WAITS") != nullptr;
-  if (dbg_on) {
-    if (!dbg_buf) cudaMalloc(&dbg_buf, 5 * 16 * sizeof(unsigned long long));
-    cudaMemsetAsync(dbg_buf, 0, 5 * 16 * sizeof(unsigned long long), s);
-    k.dbg = dbg_buf;
-  }
+  unsigned long long* dbg_buf = debug_buffer(s);
+  const bool dbg_on = dbg_buf != nullptr;
+  k.dbg = dbg_buf;
   // dynamic smem starts after the static part rounded up to 1024 B (the extern array's alignment)
   static int static_smem = -1;
   if (static_smem < 0) {
@@ -577,37 +574,64 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.notma = getenv("INFCL_DEBUG_NOTMA") != nullptr;
   auto kern = dbg_on ? pair_kernel<BWD, true> : pair_kernel<BWD, false>;
   INFCL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (prof().on) {
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, s);
-  }
+  cudaEvent_t e0 = profile_begin(s);
   kern<<<dim3(2 * g.npairs), dim3(kThreads), smem, s>>>(tmA, tmB, k);
   INFCL_CUDA_TRY(cudaGetLastError());
-  if (prof().on) {
-    cudaEventRecord(e1, s);
-    prof().ev[BWD ? 1 : 0].push_back({e0, e1});
-  }
-  if (dbg_on) {  // debug only: per-role mean wait cycles per CTA (roles: 0 TMA, 1 MMA, 2/3 epilogue lanes)
-    unsigned long long h[80];
-    cudaMemcpyAsync(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    const double nctas = 2.0 * g.npairs;
-    fprintf(stderr, "[infcl dbg] %s kernel: mean cycles/CTA total=%.0f\n", BWD ? "BWD" : "FWD", h[4 * 16 + 15] / nctas);
-    const char* names[12] = {"LOOP", "empty", "afree", "dafree", "gready", "full", "afull", "sfree", "sfull", "gfree",
-                             "dafull/sfull-commit", "S-issue"};
-    for (int role = 0; role < 4; ++role)
-      for (int t = 0; t < 12; ++t)
-        if (h[role * 16 + t])
-          fprintf(stderr, "[infcl dbg]   role %d wait %-7s %12.0f\n", role, names[t],
-                  h[role * 16 + t] / (role >= 2 ? nctas * 4 : (role == 1 ? nctas / 2 : nctas)));
-  }
+  profile_end(BWD ? 1 : 0, e0, s);
+  if (dbg_on) debug_report(BWD ? "BWD" : "FWD", g.npairs, s);
   ++launch_counter();
   return INFCL_OK;
 }
 
-infcl_status launch_pair_forward(const PassArgs& a, cudaStream_t s) { return launch_pair<false>(a, s); }
+infcl_status launch_pair_forward(const PassArgs& a, cudaStream_t s) {
+  if (wide_forward_enabled()) return launch_wide_forward(a, s);
+  return launch_pair<false>(a, s);
+}
+
+PassGeom fwd_geom(int nrows, int ncols) { return wide_forward_enabled() ? wide_geom(nrows, ncols) : pass_geom(nrows, ncols); }
+
+cudaEvent_t profile_begin(cudaStream_t s) {
+  if (!prof().on) return nullptr;
+  cudaEvent_t e0;
+  cudaEventCreate(&e0);
+  cudaEventRecord(e0, s);
+  return e0;
+}
+void profile_end(int kind, cudaEvent_t e0, cudaStream_t s) {
+  if (!e0) return;
+  cudaEvent_t e1;
+  cudaEventCreate(&e1);
+  cudaEventRecord(e1, s);
+  prof().ev[kind].push_back({e0, e1});
+}
+
+static unsigned long long*& dbg_ptr() {
+  static unsigned long long* b = nullptr;
+  return b;
+}
+unsigned long long* debug_buffer(cudaStream_t s) {
+  static const bool on = getenv("INFCL_DEBUG_WAITS") != nullptr;
+  if (!on) return nullptr;
+  if (!dbg_ptr()) cudaMalloc(&dbg_ptr(), 5 * 16 * sizeof(unsigned long long));
+  cudaMemsetAsync(dbg_ptr(), 0, 5 * 16 * sizeof(unsigned long long), s);
+  return dbg_ptr();
+}
+// debug only: per-role mean wait cycles per CTA (roles: 0 TMA, 1 MMA, 2/3 epilogue lanes)
+void debug_report(const char* name, int npairs, cudaStream_t s) {
+  unsigned long long* buf = dbg_ptr();
+  unsigned long long h[80];
+  cudaMemcpyAsync(h, buf, sizeof(h), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  const double nctas = 2.0 * npairs;
+  fprintf(stderr, "[infcl dbg] %s kernel: mean cycles/CTA total=%.0f\n", name, h[4 * 16 + 15] / nctas);
+  const char* names[12] = {"LOOP", "empty", "afree", "dafree", "gready", "full", "afull", "sfree", "sfull", "gfree",
+                           "dafull/sfull-commit", "S-issue"};
+  for (int role = 0; role < 4; ++role)
+    for (int t = 0; t < 12; ++t)
+      if (h[role * 16 + t])
+        fprintf(stderr, "[infcl dbg]   role %d wait %-7s %12.0f\n", role, names[t],
+                h[role * 16 + t] / (role >= 2 ? nctas * 4 : (role == 1 ? nctas / 2 : nctas)));
+}
 
 void profile_enable(bool on) {
   prof_clear();

@@ -212,3 +212,12 @@ def test_autograd_learnable_scale():
     loss.backward()
     _, _, ref = oracle.backward(I, T, 14.2857, 1.0, want_ds=True)
     assert abs(s.grad.item() - ref) <= 2e-3 * abs(ref) + 1e-6, (s.grad.item(), ref)
+
+
+@pytest.mark.parametrize("b,d", [(300, 128), (4096, 512), (2048, 768)])
+def test_parity_narrow_forward_kernel(b, d, monkeypatch):
+    """The narrow forward kernel (128 resident rows per pair, M=128 MMAs) stays
+    parity-green behind INFCL_FWD_NARROW (the default forward is the wide M=256 kernel)."""
+    monkeypatch.setenv("INFCL_FWD_NARROW", "1")
+    I, T = make_features(b, d, seed=21, dist="paired")
+    check_all(I, T, 14.2857)
