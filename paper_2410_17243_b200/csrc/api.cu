@@ -296,29 +296,35 @@ infcl_status bwd_step(Rank& R, const __nv_bfloat16* rowsA, const float* lse_rows
   return launch_pair_backward(a, st);
 }
 
-// ---- row-chunked single-rank pieces (the host end-to-end entry pipelines PCIe copies against them)
-// forward over stationary rows [r0, r1) of the own block: row partials into rstate, column partials merged
-// into cstate(0) right after the launch (so the slots can be reused by the next chunk)
-infcl_status fwd_chunk(Rank& R, int r0, int r1, float* diag, cudaStream_t st) {
+// ---- blocked single-rank pieces (the host end-to-end entry pipelines PCIe copies against them)
+// forward over the block (stationary rows [r0, r1) of I) x (columns [c0, c1) of T) of the own pair: row
+// partials merged into rstate right after the launch; column partials accumulate in the (pre-initialised,
+// global-column) slots and are merged once by fwd_blocks_finish
+void fwd_blocks_begin(Rank& R, cudaStream_t st) {
+  launch_init_state(R.slots(), (int)(2LL * R.L.g.npairs * R.L.slot_ld), st);
+}
+infcl_status fwd_block(Rank& R, int r0, int r1, int c0, int c1, float* diag, cudaStream_t st) {
   PassArgs a{};
   a.A = R.A + (size_t)r0 * R.L.dk;
-  a.B = R.B;
+  a.B = R.B + (size_t)c0 * R.L.dk;
   a.nrows = r1 - r0;
-  a.ncols = R.L.bs;
+  a.ncols = c1 - c0;
   a.dk = a.ld = R.L.dk;
   a.scale = R.s;
-  a.diag_on = 1;
-  a.row_off = r0;
-  a.col_slots = R.slots();
+  a.diag_on = std::max(r0, c0) < std::min(r1, c1) ? 1 : 0;
+  a.row_off = r0 - c0;
+  a.slots_merge = 1;
+  a.col_slots = R.slots() + c0;
   a.slot_ld = R.L.slot_ld;
   a.row_parts = R.rparts();
   a.diag_out = diag + r0;
   infcl_status s = launch_pair_forward(a, st);
   if (s) return s;
-  const PassGeom g = fwd_geom(a.nrows, a.ncols);
-  launch_merge_rows(R.rparts(), R.rstate() + r0, a.nrows, g, st);
-  launch_merge_cols(R.slots(), R.L.slot_ld, R.cstate(0), R.L.bs, g, st);
+  launch_merge_rows(R.rparts(), R.rstate() + r0, a.nrows, fwd_geom(a.nrows, a.ncols), st);
   return INFCL_OK;
+}
+void fwd_blocks_finish(Rank& R, cudaStream_t st) {
+  launch_merge_cols(R.slots(), R.L.slot_ld, R.cstate(0), R.L.bs, R.L.g, st, /*all_valid=*/true);
 }
 
 // dT pass over stationary rows [r0, r1) of T (own block of I streamed), then its exact diagonal term
@@ -684,18 +690,40 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
   // the whole block).
   const int nch = (dt == INFCL_BF16 && b >= 32768) ? 4 : 1;
   const int64_t chunk = ((b + nch - 1) / nch + 127) / 128 * 128;
+  const int64_t thalf = ((b + 1) / 2 + 255) / 256 * 256;  // the forward also splits T in two column halves
+  auto rows_of = [&](int k, int64_t len, int64_t& r0, int64_t& r1) {
+    r0 = std::min<int64_t>(b, k * len);
+    r1 = std::min<int64_t>(b, r0 + len);
+  };
   INFCL_CUDA_TRY(cudaEventRecord(evs[0], st));  // scratch is free once prior work on `st` is done
   INFCL_CUDA_TRY(cudaStreamWaitEvent(cin, evs[0], 0));
   INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[0], 0));
-  INFCL_CUDA_TRY(cudaMemcpyAsync(T, T_host, (size_t)b * row_bytes, cudaMemcpyHostToDevice, cin));
-  INFCL_CUDA_TRY(cudaEventRecord(evs[1], cin));
-  for (int k = 0; k < nch; ++k) {
-    const int64_t r0 = std::min<int64_t>(b, k * chunk), r1 = std::min<int64_t>(b, r0 + chunk);
+  auto copy_in = [&](void* dst, const void* src, int64_t r0, int64_t r1) -> infcl_status {
     if (r1 > r0)
-      INFCL_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(I) + r0 * row_bytes,
-                                     static_cast<const uint8_t*>(I_host) + r0 * row_bytes, (r1 - r0) * row_bytes,
+      INFCL_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + r0 * row_bytes,
+                                     static_cast<const uint8_t*>(src) + r0 * row_bytes, (r1 - r0) * row_bytes,
                                      cudaMemcpyHostToDevice, cin));
-    INFCL_CUDA_TRY(cudaEventRecord(evs[2 + k], cin));
+    return INFCL_OK;
+  };
+  if (nch == 1) {
+    TRY(copy_in(T, T_host, 0, b));
+    TRY(copy_in(I, I_host, 0, b));
+    INFCL_CUDA_TRY(cudaEventRecord(evs[2], cin));
+  } else {  // copy order T0, I0, T1, I1, I2, I3: the first forward block starts after 3/8 of the input bytes
+    int64_t r0, r1;
+    rows_of(0, thalf, r0, r1);
+    TRY(copy_in(T, T_host, r0, r1));
+    INFCL_CUDA_TRY(cudaEventRecord(evs[1], cin));
+    for (int k = 0; k < nch; ++k) {
+      rows_of(k, chunk, r0, r1);
+      TRY(copy_in(I, I_host, r0, r1));
+      INFCL_CUDA_TRY(cudaEventRecord(evs[2 + k], cin));
+      if (k == 0) {
+        rows_of(1, thalf, r0, r1);
+        TRY(copy_in(T, T_host, r0, r1));
+        INFCL_CUDA_TRY(cudaEventRecord(evs[7], cin));
+      }
+    }
   }
   launch_set_scalar(lg + 1, grad_loss, st);
   if (nch == 1) {
@@ -715,12 +743,19 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     TRY(prepare_rank(R, I, T, dt, b, d, s, 1, ws, st));
     INFCL_CUDA_TRY(cudaMemsetAsync(R.acc(), 0, sizeof(double), st));
     TRY(fwd_begin(R, st));
-    INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[1], 0));  // all of T
+    fwd_blocks_begin(R, st);
     for (int k = 0; k < nch; ++k) {
-      const int r0 = (int)std::min<int64_t>(b, k * chunk), r1 = (int)std::min<int64_t>(b, r0 + chunk);
+      int64_t r0, r1;
+      rows_of(k, chunk, r0, r1);
       INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[2 + k], 0));  // rows [r0, r1) of I
-      if (r1 > r0) TRY(fwd_chunk(R, r0, r1, dg, st));
+      for (int h = 0; h < 2; ++h) {
+        int64_t c0, c1;
+        rows_of(h, thalf, c0, c1);
+        INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[h == 0 ? 1 : 7], 0));  // columns [c0, c1) of T
+        if (r1 > r0 && c1 > c0) TRY(fwd_block(R, (int)r0, (int)r1, (int)c0, (int)c1, dg, st));
+      }
     }
+    fwd_blocks_finish(R, st);
     fwd_finish(R, R.cstate(0), r, c, dg, R.acc(), st);
     launch_loss_write(R.acc(), lg, b, st);
     INFCL_CUDA_TRY(cudaEventRecord(evs[8], st));

@@ -59,26 +59,39 @@ __global__ void merge_rows_kernel(const float2* __restrict__ parts, float2* __re
   state[i] = acc;
 }
 
-__global__ void merge_cols_kernel(const float2* __restrict__ slots, long long slot_ld, float2* __restrict__ state,
-                                  int ncols, int n_rb, int n_ct, int P) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= ncols) return;
-  const int ct = j / kColsPerTile;
+// Column state j merges the 2P per-CTA slot partials of column j (slots of pairs whose items never touched
+// column j's tile hold stale data and are skipped).  Block = 32 columns x 8 slot groups: group g merges slots
+// g, g+8, ... (independent loads in flight), then the 8 group partials merge in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) merge_cols_kernel(const float2* __restrict__ slots, long long slot_ld,
+                                                         float2* __restrict__ state, int ncols, int n_rb, int n_ct,
+                                                         int P, int all_valid) {
+  __shared__ float2 part[8][32];
+  const int j = blockIdx.x * 32 + threadIdx.x;
+  const int g = threadIdx.y;
   const int W = n_rb / P;
   const long long T = (long long)(n_rb - W * P) * n_ct;
-  float2 acc = state[j];
-  for (int p = 0; p < P; ++p) {
-    bool visited = W > 0;
-    if (!visited) {
-      const long long a = tail_begin(T, P, p), e = tail_begin(T, P, p + 1);
-      if (e - a >= n_ct) visited = true;
-      else if (e > a) visited = a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e;
+  float2 acc = make_float2(-INFINITY, 0.f);
+  if (j < ncols) {
+    const int ct = j / kColsPerTile;
+    for (int sl = g; sl < 2 * P; sl += 8) {
+      const int p = sl >> 1;
+      bool visited = all_valid || W > 0;
+      if (!visited) {
+        const long long a = tail_begin(T, P, p), e = tail_begin(T, P, p + 1);
+        if (e - a >= n_ct) visited = true;
+        else if (e > a) visited = a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e;
+      }
+      if (visited) acc = merge_ms(acc, slots[(long long)sl * slot_ld + j]);
     }
-    if (!visited) continue;
-    acc = merge_ms(acc, slots[(long long)(2 * p) * slot_ld + j]);
-    acc = merge_ms(acc, slots[(long long)(2 * p + 1) * slot_ld + j]);
   }
-  state[j] = acc;
+  part[g][threadIdx.x] = acc;
+  __syncthreads();
+  if (g == 0 && j < ncols) {
+    float2 a = state[j];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a = merge_ms(a, part[k][threadIdx.x]);
+    state[j] = a;
+  }
 }
 
 __global__ void finalize_lse_kernel(const float2* __restrict__ st, float* __restrict__ lse, float* __restrict__ lse2,
@@ -195,8 +208,9 @@ void launch_merge_rows(const float2* parts, float2* state, int nrows, const Pass
   ++launch_counter();
 }
 void launch_merge_cols(const float2* slots, long long slot_ld, float2* state, int ncols, const PassGeom& g,
-                       cudaStream_t s) {
-  merge_cols_kernel<<<nblk(ncols, 256), 256, 0, s>>>(slots, slot_ld, state, ncols, g.n_rb, g.n_ct, g.npairs);
+                       cudaStream_t s, bool all_valid) {
+  merge_cols_kernel<<<nblk(ncols, 32), dim3(32, 8), 0, s>>>(slots, slot_ld, state, ncols, g.n_rb, g.n_ct, g.npairs,
+                                                            all_valid ? 1 : 0);
   ++launch_counter();
 }
 void launch_finalize_lse(const float2* st, float* lse, float* lse2, int n, cudaStream_t s) {

@@ -21,7 +21,8 @@ struct PassArgs {
   int dk, ld;           // K extent (feature dim) and row stride in elements
   float scale;          // s
   int diag_on;          // B is A's own block: the positive pair of row i is column i + row_off
-  int row_off;          // global index of row 0 (a row chunk of the own block; 0 otherwise)
+  int row_off;          // diagonal: the positive pair of local row i is local column i + row_off
+  int slots_merge;      // forward: column slots are pre-initialised (-inf, 0); always merge into them
   // forward outputs (per pass / ring step)
   float2* col_slots;    // [2 * npairs][slot_ld] (m2, sigma) partials (workspace)
   long long slot_ld;
@@ -59,7 +60,7 @@ void debug_report(const char* name, int npairs, cudaStream_t s);
 void launch_init_state(float2* st, int n, cudaStream_t s);
 void launch_merge_rows(const float2* row_parts, float2* row_state, int nrows, const PassGeom& g, cudaStream_t s);
 void launch_merge_cols(const float2* col_slots, long long slot_ld, float2* col_state, int ncols, const PassGeom& g,
-                       cudaStream_t s);
+                       cudaStream_t s, bool all_valid = false);
 void launch_finalize_lse(const float2* st, float* lse, float* lse2, int n, cudaStream_t s);
 void launch_loss_partial(const float* r, const float* c, const float* diag, int n, double* acc, cudaStream_t s);
 void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s);

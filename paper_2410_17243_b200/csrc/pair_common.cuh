@@ -25,7 +25,7 @@ struct KParams {
   int sbox, stage_bytes;  // B boxes per ring stage (forward 1 = 16 KB stages, backward 2 = 32 KB) and its bytes
   long long n_items;
   float k2, scale;
-  int diag_on, row_off;
+  int diag_on, row_off, slots_merge;
   float2* col_slots;
   long long slot_ld;
   float2* row_parts;

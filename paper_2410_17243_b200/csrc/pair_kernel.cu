@@ -334,7 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         // forward: the 2 warps of a group each merge 32 of its 64 columns into the slot (prefetched here)
         float2 pre = make_float2(-INFINITY, 0.f);
-        const bool first_visit = it < p.n_ct;
+        const bool first_visit = !p.slots_merge && it < p.n_ct;
         float2* slot = p.col_slots + (long long)blockIdx.x * p.slot_ld;
         const int cm = cb + rh * 32 + lane;  // the column this lane merges
         if (!BWD && !first_visit && cm < p.ncols) pre = slot[cm];
@@ -535,6 +535,7 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.scale = a.scale;
   k.diag_on = a.diag_on;
   k.row_off = a.row_off;
+  k.slots_merge = a.slots_merge;
   k.col_slots = a.col_slots;
   k.slot_ld = a.slot_ld;
   k.row_parts = a.row_parts;

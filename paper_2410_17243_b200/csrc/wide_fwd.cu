@@ -162,7 +162,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (; it < seg_end; ++it) {
         const int ct = ct_first + (int)(it - seg_start);
         const int buf = (int)(it & 1);
-        const bool first_visit = it < p.n_ct;
+        const bool first_visit = !p.slots_merge && it < p.n_ct;
         wc.wait(&sfull[buf], (sph >> buf) & 1u, 8);
         sph ^= 1u << buf;
         tc_fence_after();
@@ -266,6 +266,7 @@ infcl_status launch_wide_forward(const PassArgs& a, cudaStream_t s) {
   k.scale = a.scale;
   k.diag_on = a.diag_on;
   k.row_off = a.row_off;
+  k.slots_merge = a.slots_merge;
   k.col_slots = a.col_slots;
   k.slot_ld = a.slot_ld;
   k.row_parts = a.row_parts;

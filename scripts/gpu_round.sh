@@ -7,6 +7,6 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo "bench rc=$?" >> gpurun_out/bench_${TAG}.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
    python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_bench_${TAG}.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:pair_kernel -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pair_kernel|wide_fwd" -c 2 \
    -o gpurun_out/prof_${TAG} -f python scripts/prof_step.py > gpurun_out/ncu_full_${TAG}.log 2>&1
 echo done

@@ -123,3 +123,26 @@ def test_e2e_host_entry_chunked(b, d):
     rdT = oracle.sampled_row_grads(T, I, S, ref["c"], ref["r"], rows)
     assert rel_norm(dI.numpy()[rows], rdI) <= 2e-3
     assert rel_norm(dT.numpy()[rows], rdT) <= 2e-3
+
+
+@pytest.mark.parametrize("b", [256 * 74 + 300, 256 * 74 * 2 + 4000])
+def test_wide_forward_waves_and_tail(b):
+    """Row counts that give the wide forward (256 rows per pair) one / two full waves of 74 pairs plus a ragged
+    tail split across pairs (Sched tail ranges, row-partial tail slots): every r_j, c_j and the loss exact
+    against the streamed fp64 oracle, plus the backward's sampled gradient rows."""
+    d = 64
+    I, T = make_features(b, d, seed=23, dist="paired")
+    Id, Td = I.cuda(), T.cuda()
+    loss, r, c, dg = K.infcl_forward(Id, Td, b, S)
+    dI, dT = K.infcl_backward(Id, Td, b, S, r, c, dg, torch.tensor(1.0, device="cuda"))
+    torch.cuda.synchronize()
+    ref = oracle.streamed_forward(I, T, S, chunk=4096)
+    assert abs(loss.item() - ref["loss"]) <= 1e-4 * abs(ref["loss"])
+    assert np.abs(r.cpu().numpy() - ref["r"]).max() <= 2e-3
+    assert np.abs(c.cpu().numpy() - ref["c"]).max() <= 2e-3
+    assert np.abs(dg.cpu().numpy() - ref["diag"]).max() <= 2e-3
+    rows = stratified_rows(b, 64)
+    rows = np.unique(np.concatenate([rows, [256 * 74 - 1, 256 * 74, b - 300, b - 1]]))
+    rows = rows[rows < b]
+    assert rel_norm(dI.cpu().numpy()[rows], oracle.sampled_row_grads(I, T, S, ref["r"], ref["c"], rows)) <= 2e-3
+    assert rel_norm(dT.cpu().numpy()[rows], oracle.sampled_row_grads(T, I, S, ref["c"], ref["r"], rows)) <= 2e-3
