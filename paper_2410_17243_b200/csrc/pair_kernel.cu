@@ -195,11 +195,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t ad0 = smem_desc_sw128(smem_u32(sStage + stage * p.stage_bytes), kBoxB, 1024);  // MN-major B_C^T
             const uint64_t bd0 = smem_desc_sw128(smem_u32(sG + jc * 2 * kBox), 16, 1024);           // K-major G
             const uint32_t dD = tbase + 128 + tc * 128;
-            umma_bf16_warp<2>(dD, ad0, bd0, idD, (first && jc == 0) ? 0u : 1u);
-#pragma unroll
-            for (int k = 1; k < 8; ++k)
-              umma_bf16_warp<2>(dD, ad0 + (uint64_t)(k * (2048 >> 4)),
-                                bd0 + (uint64_t)((k >> 2) * (kBox >> 4) + (k & 3) * 2), idD, 1u);
+            umma_stage_dA_pair<(kBox >> 4)>(dD, (uint32_t)ad0, (uint32_t)bd0, idD, (first && jc == 0) ? 0u : 1u);
             umma_commit_pair_mc_warp(&empty[stage], 0x3);
             advance();
           }

@@ -267,6 +267,33 @@ __device__ __forceinline__ void umma_stage_pair(uint32_t d_tmem, uint32_t a_lo, 
 #undef INFCL_STEP
 #undef INFCL_MMA2
 }
+// One ring stage of the backward's dA GEMM (dA^T += B_C^T G^T) in a single asm block: 8 MMAs over K = 128
+// columns j; the MN-major A operand (B_C^T) advances by 16 rows of j = 2048 B (128 in the >>4 field) per MMA,
+// the K-major B operand (G) by 32 B within its 64-column box and to the second box (+kBox = 512) after 4.
+// Both descriptors have the high word 0x40004040 (SBO 1024 B, version 1, SWIZZLE_128B); the MN-major one
+// carries LBO in its low word.  The first MMA accumulates iff `accumulate`.
+template <int BOX2>
+__device__ __forceinline__ void umma_stage_dA_pair(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
+                                                   uint32_t accumulate) {
+#define INFCL_MMA2(P) "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, " P ";\n\t"
+#define INFCL_STEP(DA, DB) "add.u32 al, %1, " DA ";\n\tadd.u32 bl, %2, " DB ";\n\tmov.b64 a, {al, hi};\n\tmov.b64 b, {bl, hi};\n\t"
+  asm volatile(
+      "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a, b;\n\t.reg .b32 al, bl, hi;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\tmov.b32 hi, 0x40004040;\n\t"
+      INFCL_STEP("0", "0") INFCL_MMA2("p")
+      INFCL_STEP("128", "2") INFCL_MMA2("t")
+      INFCL_STEP("256", "4") INFCL_MMA2("t")
+      INFCL_STEP("384", "6") INFCL_MMA2("t")
+      INFCL_STEP("512", "%5") INFCL_MMA2("t")
+      INFCL_STEP("640", "%6") INFCL_MMA2("t")
+      INFCL_STEP("768", "%7") INFCL_MMA2("t")
+      INFCL_STEP("896", "%8") INFCL_MMA2("t")
+      "}" ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate),
+      "n"(BOX2), "n"(BOX2 + 2), "n"(BOX2 + 4), "n"(BOX2 + 6)
+      : "memory");
+#undef INFCL_STEP
+#undef INFCL_MMA2
+}
 __device__ __forceinline__ void umma_commit_pair_mc_warp(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
