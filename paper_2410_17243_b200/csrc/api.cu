@@ -689,7 +689,11 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
   // computes (dI is copied out during the whole dT pass).  fp32 inputs run unchunked (their bf16 split needs
   // the whole block).
   const int nch = (dt == INFCL_BF16 && b >= 32768) ? 4 : 1;
-  const int64_t chunk = ((b + nch - 1) / nch + 127) / 128 * 128;
+  // chunk boundaries (eighths of b, 128-row aligned): the forward's first I chunk is small (its copy is exposed),
+  // the dT pass's last chunk is small (its copy-out is exposed)
+  auto at8 = [&](int e) { return std::min<int64_t>(b, (b * e / 8 + 127) / 128 * 128); };
+  const int64_t fwd_cut[5] = {0, at8(1), at8(4), at8(6), b};
+  const int64_t dT_cut[5] = {0, at8(3), at8(5), at8(7), b};
   const int64_t thalf = ((b + 1) / 2 + 255) / 256 * 256;  // the forward also splits T in two column halves
   auto rows_of = [&](int k, int64_t len, int64_t& r0, int64_t& r1) {
     r0 = std::min<int64_t>(b, k * len);
@@ -715,7 +719,8 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     TRY(copy_in(T, T_host, r0, r1));
     INFCL_CUDA_TRY(cudaEventRecord(evs[1], cin));
     for (int k = 0; k < nch; ++k) {
-      rows_of(k, chunk, r0, r1);
+      r0 = fwd_cut[k];
+      r1 = fwd_cut[k + 1];
       TRY(copy_in(I, I_host, r0, r1));
       INFCL_CUDA_TRY(cudaEventRecord(evs[2 + k], cin));
       if (k == 0) {
@@ -745,8 +750,7 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     TRY(fwd_begin(R, st));
     fwd_blocks_begin(R, st);
     for (int k = 0; k < nch; ++k) {
-      int64_t r0, r1;
-      rows_of(k, chunk, r0, r1);
+      const int64_t r0 = fwd_cut[k], r1 = fwd_cut[k + 1];
       INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[2 + k], 0));  // rows [r0, r1) of I
       for (int h = 0; h < 2; ++h) {
         int64_t c0, c1;
@@ -770,7 +774,7 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     INFCL_CUDA_TRY(cudaMemcpyAsync(dI_host, dI, (size_t)b * d * 4, cudaMemcpyDeviceToHost, cout));
     INFCL_CUDA_TRY(cudaMemsetAsync(dT, 0, (size_t)b * d * 4, st));
     for (int k = 0; k < nch; ++k) {
-      const int r0 = (int)std::min<int64_t>(b, k * chunk), r1 = (int)std::min<int64_t>(b, r0 + chunk);
+      const int r0 = (int)dT_cut[k], r1 = (int)dT_cut[k + 1];
       if (r1 <= r0) continue;
       TRY(bwd_dT_chunk(R, r0, r1, dg, r, c, lg + 1, dT, st));
       INFCL_CUDA_TRY(cudaEventRecord(evs[12 + k], st));

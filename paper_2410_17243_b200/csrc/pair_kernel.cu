@@ -62,7 +62,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* sStage = sG + (BWD ? 4 * kBox : 0);
 
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
-  constexpr int kNB = BWD ? 1 : 4;  // S buffers in TMEM (forward: 4 x 128 columns, MMA runs up to 3 tiles ahead)
+  // S buffers in TMEM: forward 4 x 128 columns (MMA up to 3 tiles ahead); backward one 128-column buffer in front
+  // of the dA accumulator (a second one where TMEM allows, d <= 512, measured 1-3 % slower: DESIGN.md perf log)
+  constexpr int kNB = BWD ? 1 : 4;
   __shared__ __align__(8) uint64_t afull, afree, sfull[kNB], sfree[kNB], gready, gfree, dafull, dafree;
   __shared__ uint32_t tmem_base;
   __shared__ __align__(16) float2 xch[2][4][2][64];  // forward column partials of a group's 2 warps (x tile parity)

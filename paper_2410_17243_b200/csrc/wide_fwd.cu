@@ -193,11 +193,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           float2(*xb)[4][64] = xch[cctr & 1];
           *reinterpret_cast<float4*>(&xb[u][q][2 * lane]) = cs;
           named_bar_sync(2 + u, 128);
-          if (lane < 16) {
-            const int c = q * 16 + lane;
-            float2 a = merge2(merge2(xb[u][0][c], xb[u][1][c]), merge2(xb[u][2][c], xb[u][3][c]));
-            if (!first_visit) a = merge2(pre, a);
-            if (cm < p.ncols) slot[cm] = a;
+          {  // lanes 0-15 merge row quarters 0,1 and lanes 16-31 quarters 2,3 of column q*16 + (lane & 15)
+            const int c = q * 16 + (lane & 15), hq = lane >> 4;
+            float2 a = merge2(xb[u][2 * hq][c], xb[u][2 * hq + 1][c]);
+            float2 o;
+            o.x = __shfl_xor_sync(0xffffffffu, a.x, 16);
+            o.y = __shfl_xor_sync(0xffffffffu, a.y, 16);
+            a = merge2(a, o);
+            if (lane < 16) {
+              if (!first_visit) a = merge2(pre, a);
+              if (cm < p.ncols) slot[cm] = a;
+            }
           }
           ++cctr;
         }

@@ -115,9 +115,9 @@ def test_e2e_host_entry_chunked(b, d):
     ref = oracle.streamed_forward(I, T, S, chunk=4096)
     assert abs(loss.item() - ref["loss"]) <= 1e-4 * abs(ref["loss"])
     rows = stratified_rows(b, 96)
-    # chunk boundaries (the row offset of each chunk's diagonal) are in the sample
-    chunk = ((b + 3) // 4 + 127) // 128 * 128
-    rows = np.unique(np.concatenate([rows, [chunk - 1, chunk, 2 * chunk, 3 * chunk - 1, 3 * chunk]]))
+    # block / chunk boundaries (eighths of b, 128-aligned; T halves) are in the sample
+    cuts = [min(b, (b * e // 8 + 127) // 128 * 128) for e in range(1, 8)]
+    rows = np.unique(np.concatenate([rows, [x for c in cuts for x in (c - 1, c)]]))
     rows = rows[rows < b]
     rdI = oracle.sampled_row_grads(I, T, S, ref["r"], ref["c"], rows)
     rdT = oracle.sampled_row_grads(T, I, S, ref["c"], ref["r"], rows)
