@@ -555,3 +555,81 @@ extern "C" int infcl_diag_walk2(int tiles, int KB, int ns, int mode, int ncluste
   infcl::probe_walk2_kernel<<<2 * nclusters, 320, smem>>>(tiles, KB, ns, mode, out);
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : -3;
 }
+
+// ------------------------------------------------------------------ TMA path probe 2 (diagnostic)
+// Per-SM streaming rate of a ring of `ns` 32-KB stages (consumer releases on arrival), by copy flavour:
+// mode 0: two 2D tensor boxes [64 x 128 rows] SW128 (the kernels' path); mode 1: two 1D bulk copies of 16 KB
+// (cp.async.bulk, contiguous source = pre-swizzled tile images); mode 2: one 1D bulk copy of 32 KB.
+namespace infcl {
+__global__ void __launch_bounds__(64, 1)
+    probe_tma2_kernel(const __grid_constant__ CUtensorMap tb, const uint8_t* src, long long src_bytes, int nrows,
+                      int mode, int ns, int iters, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint64_t full[8], empty[8];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ns; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const long long t0 = clock64();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    uint32_t ph = 0;
+    int row = (blockIdx.x * 997) % (nrows - 256);
+    long long off = ((long long)blockIdx.x * 1000003LL * 16) % (src_bytes - 65536);
+    off &= ~15LL;
+    for (int i = 0; i < iters; ++i) {
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_arrive_expect_tx(&full[s], 32768);
+      uint8_t* dst = smem_raw + s * 32768;
+      if (mode == 0) {
+        const int col = (i & 7) * 64;
+        tma_load_2d(dst, &tb, &full[s], col, row);
+        tma_load_2d(dst + 16384, &tb, &full[s], col, row + 128);
+        row += 256;
+        if (row >= nrows - 256) row -= nrows - 512;
+      } else {
+        const int pieces = mode == 1 ? 2 : 1, sz = 32768 / pieces;
+        for (int k = 0; k < pieces; ++k)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(dst + k * sz)),
+              "l"(src + off + k * sz), "r"(sz), "r"(smem_u32(&full[s]))
+              : "memory");
+        off += 32768;
+        if (off + 32768 > src_bytes) off = 0;
+      }
+      if (++s == ns) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (threadIdx.x == 32) {
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < iters; ++i) {
+      mbar_wait(&full[s], ph);
+      mbar_arrive(&empty[s]);
+      if (++s == ns) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    out[blockIdx.x] = clock64() - t0;
+  }
+}
+}  // namespace infcl
+
+extern "C" int infcl_diag_tma_rate2(const void* X, int nrows, int d, int mode, int ns, int iters, int nblocks,
+                                    long long* out) {
+  CUtensorMap b;
+  if (make_tmap_bf16(&b, X, nrows, d, d, 64, 128)) return -1;
+  if (ns < 1 || ns > 6) return -2;
+  cudaFuncSetAttribute(infcl::probe_tma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 32768);
+  infcl::probe_tma2_kernel<<<nblocks, 64, 6 * 32768>>>(b, static_cast<const uint8_t*>(X), (long long)nrows * d * 2,
+                                                         nrows, mode, ns, iters, out);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : -3;
+}

@@ -75,6 +75,14 @@ def test_parity_independent(b, d, s):
     check_all(I, T, s)
 
 
+@pytest.mark.parametrize("b,d", [(520, 40), (1500, 200), (700, 456), (2100, 712)])
+def test_parity_ragged_feature_dim(b, d):
+    """d not a multiple of the 64-wide K block: the last K block is zero-filled by TMA (both operands), and for
+    the backward the last 256-wide d-chunk of the dA accumulator is partial."""
+    I, T = make_features(b, d, seed=b + 7 * d, dist="paired")
+    check_all(I, T, 14.2857)
+
+
 @pytest.mark.parametrize("s", [0.0, 100.0])
 def test_parity_scales(s):
     I, T = make_features(1024, 512, seed=5, dist="paired")
@@ -165,6 +173,10 @@ def test_errors():
     I, T = make_features(64, 32, seed=1)
     with pytest.raises(InfclError):
         K.infcl_forward(I.cuda(), T.cuda(), 64, float("nan"))
+    with pytest.raises(InfclError):  # empty batch
+        K.infcl_forward(I[:0].cuda(), T[:0].cuda(), 0, 1.0)
+    with pytest.raises(InfclError):  # negative logit scale
+        K.infcl_forward(I.cuda(), T.cuda(), 64, -1.0)
 
 
 def test_forward_exact_fallback_adversarial_columns():
