@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -676,13 +677,26 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
   const size_t wsb = infcl_workspace_bytes(b, d, 1, dt);
   TRY(validate(I_host, T_host, dt, b, d, s, 0, 1, ws, wsb, wsb));
   // side streams: host->device copies (cin) and device->host copies (cout) overlap the kernels on `st`
-  static cudaStream_t cin = nullptr, cout = nullptr;
-  static cudaEvent_t evs[24];
-  if (!cin) {
-    INFCL_CUDA_TRY(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
-    INFCL_CUDA_TRY(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
-    for (auto& e : evs) INFCL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // side streams and events, created once per device (the call synchronises before returning, so one set per
+  // device suffices; a mutex serialises concurrent host threads that share a device)
+  struct CopyCtx {
+    cudaStream_t cin = nullptr, cout = nullptr;
+    cudaEvent_t evs[24] = {};
+    std::mutex mu;
+  };
+  static CopyCtx ctxs[64];
+  int dev = 0;
+  INFCL_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(INFCL_ERR_UNSUPPORTED, "device index above 63");
+  CopyCtx& cx = ctxs[dev];
+  std::lock_guard<std::mutex> lock(cx.mu);
+  if (!cx.cin) {
+    INFCL_CUDA_TRY(cudaStreamCreateWithFlags(&cx.cin, cudaStreamNonBlocking));
+    INFCL_CUDA_TRY(cudaStreamCreateWithFlags(&cx.cout, cudaStreamNonBlocking));
+    for (auto& e : cx.evs) INFCL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
+  cudaStream_t cin = cx.cin, cout = cx.cout;
+  cudaEvent_t* evs = cx.evs;
   const size_t row_bytes = (size_t)d * esz;
   // bf16: the stationary side is processed in row chunks so that (1) the forward starts on the first chunk of
   // I while the rest is still in flight and (2) each finished chunk of dT is copied out while the next one
