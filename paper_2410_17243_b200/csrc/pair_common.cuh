@@ -26,6 +26,7 @@ struct KParams {
   long long n_items;
   float k2, scale;
   int diag_on, row_off, slots_merge;
+  int pair_commit;  // even ring: one tcgen05.commit per two stages (empty[even] releases the pair)
   float2* col_slots;
   long long slot_ld;
   float2* row_parts;
@@ -134,6 +135,20 @@ struct WaitClock {
   }
 };
 
+
+// Ring stage release / acquire with optional pairing: a commit costs the tensor pipe a bubble, so with an even
+// number of stages the MMA warp commits once per two stages (to empty[s-1] after odd stage s; the commit fires
+// when all prior MMAs complete, i.e. it covers both) and the producer waits only before even stages.
+// (scripts/walk_probe5.py: -6 % cycles per MMA in the loop-structure probe.)
+__device__ __forceinline__ void ring_release(uint64_t* empty, int stage, int pair_commit) {
+  if (!pair_commit) umma_commit_pair_mc_warp(&empty[stage], 0x3);
+  else if (stage & 1) umma_commit_pair_mc_warp(&empty[stage - 1], 0x3);
+}
+template <bool DBG>
+__device__ __forceinline__ void ring_acquire(WaitClock<DBG>& wc, uint64_t* empty, int stage, uint32_t ph,
+                                             int pair_commit) {
+  if (!pair_commit || !(stage & 1)) wc.wait(&empty[stage], ph ^ 1, 1);
+}
 
 // Forward statistics of one 64-column chunk of an S tile held by this warp in the tcgen05.ld 16x256b layout:
 // t0 = lane & 3, t1 = lane >> 2; value v[eta*32 + rho*4 + kap*2 + c] is row rowbase + 16*eta + 8*kap (launch-

@@ -113,7 +113,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t ph = 0, aph = 0;
       auto load_stage = [&](int c0a, int c1a, int c0b, int c1b) {
-        wc.wait(&empty[stage], ph ^ 1, 1);
+        ring_acquire(wc, empty, stage, ph, p.pair_commit);
         if (DBG && p.notma) {
           if (cta == 0) mbar_arrive(&full[stage]);
         } else {
@@ -198,7 +198,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t bd0 = smem_desc_sw128(smem_u32(sG + jc * 2 * kBox), 16, 1024);           // K-major G
             const uint32_t dD = tbase + 128 + tc * 128;
             umma_stage_dA_pair<(kBox >> 4)>(dD, (uint32_t)ad0, (uint32_t)bd0, idD, (first && jc == 0) ? 0u : 1u);
-            umma_commit_pair_mc_warp(&empty[stage], 0x3);
+            ring_release(empty, stage, p.pair_commit);
             advance();
           }
         }
@@ -229,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               umma_stage_pair<true, (kBox >> 4), (kBoxB >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
             else  // one box per stage, or the half-used last stage of an odd number of 64-d blocks
               umma_stage_pair<false, 0, 0>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
-            umma_commit_pair_mc_warp(&empty[stage], 0x3);
+            ring_release(empty, stage, p.pair_commit);
             if (DBG) wc.acc[11] += clock64() - t_is;
             advance();
           }
@@ -562,6 +562,7 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   if (const char* e = getenv("INFCL_STAGES")) ns = std::max(2, std::min(ns, atoi(e)));
   if (ns < 2) return fail(INFCL_ERR_SHAPE, "feature dim too large for the smem budget");
   k.n_stages = ns;
+  k.pair_commit = (ns % 2 == 0 && !getenv("INFCL_NO_PAIR_COMMIT")) ? 1 : 0;
   const size_t smem = fixed + (size_t)ns * k.stage_bytes;
 
   CUtensorMap tmA, tmB;

@@ -479,13 +479,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       const uint32_t dS = tbase + buf * (wide ? 256 : 128);
       for (int kc = 0; kc < KC; ++kc) {
         if (mode & 16) mbar_wait(&full[stage], ph);
-        else if (n >= ns && !(mode & 128)) mbar_wait(&empty[stage], ph ^ 1);
+        else if (n >= ns && !(mode & 128)) mbar_wait(&empty[(mode & 1024) ? (stage & ~1) : stage], ph ^ 1);
         tc_fence_after();
         const uint64_t ad0 = smem_desc_sw128(smem_u32(sA + 2 * kc * (wide ? 16384 : 8192)), 16, 1024);
         const uint64_t bd0 = smem_desc_sw128(smem_u32(sB + stage * 32768), 16, 1024);
         if (wide) umma_stage_pair<true, (16384 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
         else umma_stage_pair<true, (8192 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
-        if (!(mode & 256)) {
+        if (mode & 1024) {  // ONE commit per two stages: empty[even] covers the pair
+          if (stage & 1) umma_commit_pair_mc_warp(&empty[stage - 1], 0x3);
+        } else if (!(mode & 256)) {
           umma_commit_pair_mc_warp(&empty[stage], 0x3);
         } else if (stage & 1) {  // release two stages per commit pair, issued back to back at the odd stage
           umma_commit_pair_mc_warp(&empty[stage - 1], 0x3);
@@ -512,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       int stage = 0;
       uint32_t ph = 0;
       for (long long n = 0; n < nst; ++n) {
-        mbar_wait(&empty[stage], ph ^ 1);
+        if (!(mode & 1024) || !(stage & 1)) mbar_wait(&empty[(mode & 1024) ? (stage & ~1) : stage], ph ^ 1);
         if (cta == 0) mbar_arrive(&full[stage]);
         if (++stage == ns) {
           stage = 0;

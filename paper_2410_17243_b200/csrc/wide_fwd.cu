@@ -90,7 +90,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int ct = ct0; it < seg_end; ++it, ++ct) {  // a segment's column tiles are consecutive
           const int b_row = ct * kColsPerTile + (int)cta * 128;
           for (int kb = 0; kb < p.KB; ++kb) {
-            wc.wait(&empty[stage], ph ^ 1, 1);
+            ring_acquire(wc, empty, stage, ph, p.pair_commit);
             if (DBG && p.notma) {
               if (cta == 0) mbar_arrive(&full[stage]);
             } else {
@@ -129,7 +129,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t st = smem_u32(sStage + stage * kWStage);
           umma_stage_pair<false, 0, 0>(dS, (uint32_t)smem_desc_sw128(st, 16, 1024),
                                        (uint32_t)smem_desc_sw128(st + kBoxB, 16, 1024), idS, kb != 0);
-          umma_commit_pair_mc_warp(&empty[stage], 0x3);
+          ring_release(empty, stage, p.pair_commit);
           if (DBG) wc.acc[11] += clock64() - t_is;
           if (++stage == p.n_stages) {
             stage = 0;
@@ -289,6 +289,7 @@ infcl_status launch_wide_forward(const PassArgs& a, cudaStream_t s) {
   int ns = (int)std::min<long long>(kMaxStages, budget / kWStage);
   if (const char* e = getenv("INFCL_STAGES")) ns = std::max(2, std::min(ns, atoi(e)));
   k.n_stages = ns;
+  k.pair_commit = (ns % 2 == 0 && !getenv("INFCL_NO_PAIR_COMMIT")) ? 1 : 0;
   const size_t smem = (size_t)ns * kWStage;
   CUtensorMap tmA, tmB;
   infcl_status st = make_tmap_bf16(&tmA, a.A, a.nrows, a.dk, a.ld, 64, 128);
