@@ -60,3 +60,31 @@ def test_product_path_does_not_import_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(root, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_binding_rejects_host_tensors_and_shape_mismatch():
+    """The Python binding is marshalling only: host tensors never reach a CPU fallback (there is none)."""
+    import pytest
+    import torch
+    from paper_2410_17243_b200 import loss as K
+    I = torch.zeros(64, 32, dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="CUDA"):
+        K.infcl_forward(I, I, 64, 1.0)
+    with pytest.raises((ValueError, TypeError)):
+        K._check_features(torch.zeros(64, 32), torch.zeros(64, 16))
+    with pytest.raises(TypeError):
+        K._dtype_code(torch.zeros(4, 8, dtype=torch.float16))
+
+
+def test_workspace_and_e2e_scratch_sizes():
+    """Workspace grows linearly in b (O(b d) per GPU, SURVEY 8(d) memory) and is 0 for invalid shapes."""
+    lib = L.lib()
+    w1 = lib.infcl_workspace_bytes(65536, 512, 1, 0)
+    w2 = lib.infcl_workspace_bytes(131072, 512, 1, 0)
+    assert 1.9 < w2 / w1 < 2.1
+    # a ring rank also holds two travelling blocks (2 b_s d bf16) and their LSE vectors
+    assert lib.infcl_workspace_bytes(65536, 512, 8, 0) >= 2 * (65536 // 8) * 512 * 2
+    assert lib.infcl_workspace_bytes(0, 512, 1, 0) == 0
+    s1 = lib.infcl_e2e_scratch_bytes(65536, 512, 0)
+    # e2e scratch holds the bf16 inputs, fp32 gradients, LSE vectors and the workspace
+    assert s1 >= 2 * 65536 * 512 * 2 + 2 * 65536 * 512 * 4 + w1
