@@ -83,29 +83,6 @@ __device__ __forceinline__ float2 merge2(float2 a, float2 b) {
   return make_float2(M, a.y * ex2(a.x - M) + b.y * ex2(b.x - M));
 }
 
-// Transposed butterfly reduction of 32 values per lane: afterwards lane l holds op over the 32 lanes of
-// the value originally at index l (5 rounds, 31 shuffles).
-template <bool IS_MAX>
-__device__ __forceinline__ float xreduce32(float (&t)[32], int lane) {
-#define XR_ROUND(O, N)                                                 \
-  {                                                                    \
-    const bool up = (lane & (O)) != 0;                                 \
-    _Pragma("unroll") for (int i = 0; i < (N); ++i) {                  \
-      const float send = up ? t[i] : t[i + (N)];                       \
-      const float keep = up ? t[i + (N)] : t[i];                       \
-      const float recv = __shfl_xor_sync(0xffffffffu, send, (O));      \
-      t[i] = IS_MAX ? fmaxf(keep, recv) : keep + recv;                 \
-    }                                                                  \
-  }
-  XR_ROUND(16, 16)
-  XR_ROUND(8, 8)
-  XR_ROUND(4, 4)
-  XR_ROUND(2, 2)
-  XR_ROUND(1, 1)
-#undef XR_ROUND
-  return t[0];
-}
-
 template <bool ON>
 struct WaitClock {
   // every lane of the role times its waits (a lane-dependent branch here would diverge a converged warp and
@@ -129,9 +106,11 @@ struct WaitClock {
     acc[tag] += clock64() - t0;
   }
   __device__ void flush(int role) {
-    if (!ON || !dbg || !leader) return;
-    for (int i = 0; i < 12; ++i)
-      if (acc[i]) atomicAdd(dbg + role * 16 + i, acc[i]);
+    if constexpr (ON) {
+      if (!dbg || !leader) return;
+      for (int i = 0; i < 12; ++i)
+        if (acc[i]) atomicAdd(dbg + role * 16 + i, acc[i]);
+    }
   }
 };
 
@@ -161,7 +140,7 @@ __device__ __forceinline__ void ring_acquire(WaitClock<DBG>& wc, uint64_t* empty
 __device__ __forceinline__ float4 fwd_chunk_stats(float (&v)[64], uint32_t lchunk, int rowbase, int cb,
                                                   const KParams& p, int lane, float (&mrow)[4], float (&srow)[4]) {
   const float k2 = p.k2;
-  const int t0 = lane & 3, t1 = lane >> 2;
+  const int t0 = lane & 3;
   bool rok[4];
 #pragma unroll
   for (int ri = 0; ri < 4; ++ri) rok[ri] = rowbase + 16 * (ri >> 1) + 8 * (ri & 1) < p.nrows;

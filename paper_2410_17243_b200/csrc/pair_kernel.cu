@@ -265,7 +265,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int rh = q & 1;
     const int r = rh * 32 + lane;  // row within this CTA's 64
     const int grp = h * 2 + u;     // the 2 warps (rh = 0, 1) that share these 64 columns
-    const int et = ep * 32 + lane;  // 0..255
     const uint32_t laddr = tbase + ((uint32_t)(q * 32) << 16) + u * 64;
     uint32_t sph = 0, gfph = 0, daph = 0;  // sph: phase bit of sfull[b] = bit b
     WaitClock<DBG> wc(p.dbg, lane == 0);
