@@ -126,6 +126,12 @@ infcl_status infcl_backward_virtual(const void* I, const void* T, infcl_dtype dt
  * End-to-end convenience entry (world == 1): HOST inputs and outputs, device scratch allocated by the
  * caller.  Copies I, T host->device, runs forward + backward, copies loss, dI, dT device->host, and
  * synchronises `stream` before returning.  dev_scratch must hold infcl_e2e_scratch_bytes(b, d, dt).
+ * For bf16 and b >= 32768 the copies run on library-owned side streams (one set per device, calls on the
+ * same device serialise) and are pipelined against the kernels: the forward runs in blocks (I row chunks x
+ * T column halves) as their inputs land, dI is copied out during the dT pass, and the dT pass runs in row
+ * chunks each copied out while the next computes.  Pinned host buffers are needed for the copies to overlap
+ * (pageable memory still works, synchronously).  Results equal the device entry points' up to the order
+ * of the column-LSE merges (fp32 rounding).
  * ------------------------------------------------------------------------------------------------- */
 size_t infcl_e2e_scratch_bytes(int64_t b, int d, infcl_dtype dt);
 infcl_status infcl_loss_grad_host(const void* I_host, const void* T_host, infcl_dtype dt, int64_t b, int d,
