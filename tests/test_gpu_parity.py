@@ -131,6 +131,20 @@ def test_virtual_ring_matches(world):
     check_all(I, T, 14.2857, world=world)
 
 
+@pytest.mark.parametrize("b,d,world", [(3 * 700, 128, 3), (8 * 600, 64, 8), (5 * 1024, 512, 5)])
+def test_virtual_ring_odd_and_ragged_shards(b, d, world):
+    """Odd world sizes and per-rank shards that are not multiples of the 128/256-row tiles (ragged tails in
+    every ring step, diagonal tiles at shard offsets) through the n-rank ring schedule."""
+    I, T = make_features(b, d, seed=world + b, dist="paired")
+    check_all(I, T, 14.2857, world=world)
+
+
+def test_fp32_virtual_ring():
+    """fp32 inputs (hi/lo split, 3d-wide K) through the 2-rank ring: the split runs per rank on its shard."""
+    I, T = make_features(512, 64, seed=4, dtype=torch.float32)
+    check_all(I, T, 14.2857, world=2)
+
+
 def test_b1_and_tiny():
     I, T = make_features(8, 16, seed=2)
     check_all(I, T, 3.0)
