@@ -378,7 +378,8 @@ infcl_status pass_end(Rank& R, int pass, float* out, const float* diag, const fl
     launch_combine_f32(R.dscr(), R.L.dk, out, R.L.bs, R.L.d, pass == 0 ? 0 : 1, st);
   }
   const void* Bi = pass == 0 ? R.T_orig : R.I_orig;
-  launch_diag_correction(out, R.L.d, Bi, R.L.d, R.L.f32 ? 1 : 0, diag, row_lse, col_lse, grad,
+  if (INFCL_MUTATION != 4)
+    launch_diag_correction(out, R.L.d, Bi, R.L.d, R.L.f32 ? 1 : 0, diag, row_lse, col_lse, grad,
                          (float)((double)R.s / (2.0 * (double)R.b)), R.s, R.L.bs, R.L.d, st);
   if (pass == 0) {
     if (R.L.f32) {

@@ -1,5 +1,11 @@
 // Internal (C++) interface between the ABI layer (api.cu) and the CUDA kernels.
 #pragma once
+// INFCL_MUTATION (test builds only, scripts/mutation_check.py): 1 = forward row merge drops the rescale of the
+// old running sum; 2 = backward G loses its column term; 3 = wide forward streams the wrong B column tile;
+// 4 = the exact diagonal gradient term is skipped.  The parity suite must fail for each; 0 = the product.
+#ifndef INFCL_MUTATION
+#define INFCL_MUTATION 0
+#endif
 #include <cuda.h>
 #include <cuda_runtime.h>
 

@@ -201,7 +201,7 @@ __device__ __forceinline__ float4 fwd_chunk_stats(float (&v)[64], uint32_t lchun
     const float mn = fmaxf(mrow[ri], ml[ri]);
     const float a_old = mrow[ri] == -INFINITY ? 0.f : ex2(mrow[ri] - mn);
     const float a_new = ml[ri] == -INFINITY ? 0.f : ex2(ml[ri] - mn);
-    srow[ri] = srow[ri] * a_old + acc * a_new;
+    srow[ri] = (INFCL_MUTATION == 1 ? srow[ri] : srow[ri] * a_old) + acc * a_new;
     mrow[ri] = mn;
   }
   float Rw = fmaxf(fmaxf(ml[0], ml[1]), fmaxf(ml[2], ml[3]));

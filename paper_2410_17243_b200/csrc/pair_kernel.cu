@@ -401,7 +401,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const float2 t0 = __ffma2_rn(make_float2(v[j + 0], v[j + 1]), kk, nr);
               const float2 t1 = __ffma2_rn(make_float2(v[j + 2], v[j + 3]), kk, nr);
               const float2 e0 = make_float2(ex2(t0.x), ex2(t0.y)), e1 = make_float2(ex2(t1.x), ex2(t1.y));
-              const float2 g0 = __ffma2_rn(e0, __fmul2_rn(pp, make_float2(q4.x, q4.y)), e0);
+              const float2 g0 = INFCL_MUTATION == 2 ? e0 : __ffma2_rn(e0, __fmul2_rn(pp, make_float2(q4.x, q4.y)), e0);
               const float2 g1 = __ffma2_rn(e1, __fmul2_rn(pp, make_float2(q4.z, q4.w)), e1);
               pk[j / 2] = pack_bf16(g0.x, g0.y);
               pk[j / 2 + 1] = pack_bf16(g1.x, g1.y);

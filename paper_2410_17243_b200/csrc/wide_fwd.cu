@@ -88,7 +88,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const long long seg_end = S.seg_end(it);
         const int a_row = rb * kWRows + (int)cta * 128;
         for (int ct = ct0; it < seg_end; ++it, ++ct) {  // a segment's column tiles are consecutive
-          const int b_row = ct * kColsPerTile + (int)cta * 128;
+          const int b_row = (ct + (INFCL_MUTATION == 3 && ct == 0 ? 1 : 0)) * kColsPerTile + (int)cta * 128;
           for (int kb = 0; kb < p.KB; ++kb) {
             ring_acquire(wc, empty, stage, ph, p.pair_commit);
             if (DBG && p.notma) {
