@@ -35,6 +35,7 @@ struct NcclApi {
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   bool ok = false;
 };
 
@@ -57,6 +58,7 @@ NcclApi& nccl() {
       LOAD(GroupEnd);
       LOAD(AllReduce);
       LOAD(GetErrorString);
+      LOAD(CommGetAsyncError);
 #undef LOAD
       api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.GroupStart &&
                api.GroupEnd && api.AllReduce;
@@ -404,6 +406,16 @@ infcl_status ring_exchange(infcl_comm c, const void* send, void* recv, size_t by
   INFCL_NCCL_TRY(nccl().GroupEnd());
   return INFCL_OK;
 }
+// non-blocking check for an asynchronous NCCL failure on the ring (a peer died, a network error): reported as
+// INFCL_ERR_NCCL instead of surfacing later as a hang
+infcl_status comm_async_check(infcl_comm c) {
+  if (!c || !c->comm || !nccl().CommGetAsyncError) return INFCL_OK;
+  ncclResult_t r = ncclSuccess;
+  if (nccl().CommGetAsyncError(c->comm, &r) != ncclSuccess || (r != ncclSuccess && r != ncclInProgress))
+    return fail(INFCL_ERR_NCCL, std::string("asynchronous NCCL error: ") +
+                                    (nccl().GetErrorString ? nccl().GetErrorString(r) : std::to_string(r)));
+  return INFCL_OK;
+}
 }  // namespace
 
 extern "C" size_t infcl_workspace_bytes(int64_t b, int d, int world, infcl_dtype dt) {
@@ -468,6 +480,7 @@ extern "C" infcl_status infcl_forward(infcl_comm comm, const void* I_local, cons
   INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 7), comm->stream));
   INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 7), 0));
   launch_loss_write(R.acc(), loss, b, st);
+  TRY(comm_async_check(comm));
   INFCL_CUDA_TRY(cudaGetLastError());
   return INFCL_OK;
 }
@@ -524,6 +537,7 @@ static infcl_status backward_impl(infcl_comm comm, const void* I_local, const vo
     TRY(pass_end(R, pass, out, diag, row_lse, col_lse, grad, st));
     if (pass == 0 && dI_ready) INFCL_CUDA_TRY(cudaEventRecord(dI_ready, st));  // dI final: callers may copy it out
   }
+  if (world > 1) TRY(comm_async_check(comm));
   INFCL_CUDA_TRY(cudaGetLastError());
   return INFCL_OK;
 }
