@@ -118,7 +118,7 @@ struct WaitClock {
 // Ring stage release / acquire with optional pairing: a commit costs the tensor pipe a bubble, so with an even
 // number of stages the MMA warp commits once per two stages (to empty[s-1] after odd stage s; the commit fires
 // when all prior MMAs complete, i.e. it covers both) and the producer waits only before even stages.
-// (scripts/walk_probe5.py: -6 % cycles per MMA in the loop-structure probe.)
+// (scripts/experiments/walk_probe5.py: -6 % cycles per MMA in the loop-structure probe.)
 __device__ __forceinline__ void ring_release(uint64_t* empty, int stage, int pair_commit) {
   if (!pair_commit) umma_commit_pair_mc_warp(&empty[stage], 0x3);
   else if (stage & 1) umma_commit_pair_mc_warp(&empty[stage - 1], 0x3);

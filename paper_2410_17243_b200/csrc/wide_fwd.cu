@@ -3,7 +3,7 @@
 //
 // Why a second forward kernel: the narrow pair kernel (pair_kernel.cu) keeps 128 stationary rows per pair
 // resident and issues M=128 pair MMAs (64 tensor cycles each).  Loop-structure probes (probe_walk2_kernel,
-// scripts/walk_probe4.py) show those run at 70-78 % of the tensor rate once the ring handshakes are in the
+// scripts/experiments/walk_probe4.py) show those run at 70-78 % of the tensor rate once the ring handshakes are in the
 // loop, while M=256 pair MMAs (128 cycles each) stay at 100 % with the same handshakes.  The forward has no
 // TMEM-resident accumulator besides S, so it can afford 256-row pair tiles: S (256 x 256) = A_R * B_C^T with
 // tcgen05.mma.cta_group::2 M=256 N=256 (per SM: 128 rows x 256 columns, TMEM lane = row).  The stationary

@@ -1,8 +1,8 @@
 """Loop-structure probe 5: one commit per stage vs one commit per two stages (M=128 pair MMAs, real roles)."""
 import ctypes, os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
-L = ctypes.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2410_17243_b200/libinfcl.so"))
+L = ctypes.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))), "paper_2410_17243_b200/libinfcl.so"))
 out = torch.zeros(4, dtype=torch.int64, device="cuda")
 KB, ns, tiles = 8, 4, 2000
 for rep in range(2):
