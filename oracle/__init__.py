@@ -8,7 +8,7 @@ Citations: ``P:n`` = /root/reference/PAPER.md line n, ``S:n`` = SPEC.md line n (
 Readings of ambiguous passages are listed in DESIGN.md "Readings" (Q1..Q23 of SURVEY.md 8(c)).
 
 Pinning (every function below is pinned by a ``-m "not gpu"`` test against something other than itself):
-  brute-force Python loops (tests/test_oracle_brute.py), closed forms (identical features, one-hot classes,
+  brute-force Python loops (tests/brute.py, used by tests/test_oracle_pins.py), closed forms (identical features, one-hot classes,
   codebook inputs), central finite differences, gradient invariants, swap symmetry, and the SPEC's printed
   examples (tests/golden/spec_examples.txt).  No function is "parity unpinned".
 """
