@@ -691,9 +691,9 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
   void* ws = p;
   const size_t wsb = infcl_workspace_bytes(b, d, 1, dt);
   TRY(validate(I_host, T_host, dt, b, d, s, 0, 1, ws, wsb, wsb));
-  // side streams: host->device copies (cin) and device->host copies (cout) overlap the kernels on `st`
-  // side streams and events, created once per device (the call synchronises before returning, so one set per
-  // device suffices; a mutex serialises concurrent host threads that share a device)
+  // side streams for host->device (cin) and device->host (cout) copies overlapping the kernels on `st`, with
+  // their events: created once per device (the call synchronises before returning, so one set per device
+  // suffices; a mutex serialises concurrent host threads that share a device)
   struct CopyCtx {
     cudaStream_t cin = nullptr, cout = nullptr;
     cudaEvent_t evs[24] = {};
