@@ -330,7 +330,8 @@ void fwd_blocks_finish(Rank& R, cudaStream_t st) {
   launch_merge_cols(R.slots(), R.L.slot_ld, R.cstate(0), R.L.bs, R.L.g, st, /*all_valid=*/true);
 }
 
-// dT pass over stationary rows [r0, r1) of T (own block of I streamed), then its exact diagonal term
+// dT pass over stationary rows [r0, r1) of T (own block of I streamed); dT holds its exact diagonal term already
+// (diag_init)
 infcl_status bwd_dT_chunk(Rank& R, int r0, int r1, const float* diag, const float* row_lse, const float* col_lse,
                           const float* grad, float* dT, cudaStream_t st) {
   PassArgs a{};
@@ -351,22 +352,28 @@ infcl_status bwd_dT_chunk(Rank& R, int r0, int r1, const float* diag, const floa
   a.coef_base = (float)((double)R.s / (2.0 * (double)R.b));
   infcl_status s = launch_pair_backward(a, st);
   if (s) return s;
-  launch_diag_correction(dT + (size_t)r0 * R.L.d, R.L.d,
-                         static_cast<const __nv_bfloat16*>(R.I_orig) + (size_t)r0 * R.L.d, R.L.d, 0, diag + r0,
-                         row_lse + r0, col_lse + r0, grad, a.coef_base, R.s, a.nrows, R.L.d, st);
   INFCL_CUDA_TRY(cudaGetLastError());
   return INFCL_OK;
 }
 
-infcl_status bwd_begin(Rank& R, const float* row_lse, const float* col_lse, float* dI, float* dT, cudaStream_t st) {
+// bf16: the pass output starts as its exact fp32 diagonal term (reading H7) and the pair kernel's red.add drains
+// accumulate onto it -- one write instead of a memset plus a later read-modify-write.  pass 0 (dI): B_i = T_i;
+// pass 1 (dT): B_i = I_i.  fp32 inputs accumulate into the 3d-wide scratch (zeroed) and add the term in pass_end.
+void diag_init(Rank& R, int pass, float* out, const float* diag, const float* row_lse, const float* col_lse,
+               const float* grad, cudaStream_t st) {
+  launch_diag_term(out, R.L.d, pass == 0 ? R.T_orig : R.I_orig, R.L.d, 0, diag, row_lse, col_lse, grad,
+                   (float)((double)R.s / (2.0 * (double)R.b)), R.L.bs, R.L.d, /*init=*/true, st);
+}
+
+infcl_status bwd_begin(Rank& R, const float* row_lse, const float* col_lse, const float* diag, const float* grad,
+                       float* dI, cudaStream_t st) {
   launch_scale_log2(row_lse, R.own2(0), R.L.bs, st);
   launch_scale_log2(col_lse, R.own2(1), R.L.bs, st);
   if (R.L.f32) {
     INFCL_CUDA_TRY(cudaMemsetAsync(R.dscr(), 0, (size_t)R.L.bs * R.L.dk * sizeof(float), st));
   } else {
-    INFCL_CUDA_TRY(cudaMemsetAsync(dI, 0, (size_t)R.L.bs * R.L.d * sizeof(float), st));
+    diag_init(R, 0, dI, diag, row_lse, col_lse, grad, st);
   }
-  (void)dT;
   return INFCL_OK;
 }
 
@@ -375,18 +382,12 @@ float* pass_dst(Rank& R, float* out) { return R.L.f32 ? R.dscr() : out; }
 
 infcl_status pass_end(Rank& R, int pass, float* out, const float* diag, const float* row_lse, const float* col_lse,
                       const float* grad, cudaStream_t st) {
-  // pass 0 (dI): B_i = T_i; pass 1 (dT): B_i = I_i
-  if (R.L.f32) {
+  if (R.L.f32) {  // fp32: combine the hi/lo partials, then add the diagonal term (bf16: diag_init did it)
     launch_combine_f32(R.dscr(), R.L.dk, out, R.L.bs, R.L.d, pass == 0 ? 0 : 1, st);
-  }
-  const void* Bi = pass == 0 ? R.T_orig : R.I_orig;
-  if (INFCL_MUTATION != 4)
-    launch_diag_correction(out, R.L.d, Bi, R.L.d, R.L.f32 ? 1 : 0, diag, row_lse, col_lse, grad,
-                         (float)((double)R.s / (2.0 * (double)R.b)), R.s, R.L.bs, R.L.d, st);
-  if (pass == 0) {
-    if (R.L.f32) {
-      INFCL_CUDA_TRY(cudaMemsetAsync(R.dscr(), 0, (size_t)R.L.bs * R.L.dk * sizeof(float), st));
-    }
+    const void* Bi = pass == 0 ? R.T_orig : R.I_orig;
+    launch_diag_term(out, R.L.d, Bi, R.L.d, 1, diag, row_lse, col_lse, grad,
+                     (float)((double)R.s / (2.0 * (double)R.b)), R.L.bs, R.L.d, /*init=*/false, st);
+    if (pass == 0) INFCL_CUDA_TRY(cudaMemsetAsync(R.dscr(), 0, (size_t)R.L.bs * R.L.dk * sizeof(float), st));
   }
   INFCL_CUDA_TRY(cudaGetLastError());
   return INFCL_OK;
@@ -497,7 +498,7 @@ static infcl_status backward_impl(infcl_comm comm, const void* I_local, const vo
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Rank R;
   TRY(prepare_rank(R, I_local, T_local, dt, b, d, s, world, ws, st));
-  TRY(bwd_begin(R, row_lse, col_lse, dI, dT, st));
+  TRY(bwd_begin(R, row_lse, col_lse, diag, grad, dI, st));
   const size_t blk_bytes = (size_t)R.L.bs * R.L.dk * 2, lse_bytes = (size_t)R.L.bs * sizeof(float);
   for (int pass = 0; pass < 2; ++pass) {
     // pass 0: rows I (lse r), stream (T, c) -> dI;  pass 1: rows T (lse c), stream (I, r) -> dT
@@ -508,7 +509,7 @@ static infcl_status backward_impl(infcl_comm comm, const void* I_local, const vo
     float* out = pass == 0 ? dI : dT;
     float* dst = pass_dst(R, out);
     const int ld_dst = R.L.f32 ? R.L.dk : R.L.d;
-    if (!R.L.f32 && pass == 1) INFCL_CUDA_TRY(cudaMemsetAsync(dT, 0, (size_t)R.L.bs * R.L.d * sizeof(float), st));
+    if (!R.L.f32 && pass == 1) diag_init(R, 1, dT, diag, row_lse, col_lse, grad, st);
     if (world == 1) {
       TRY(bwd_step(R, rows, rows2, own_blk, own_cols2, true, dst, ld_dst, grad, st));
     } else {
@@ -610,8 +611,8 @@ extern "C" infcl_status infcl_backward_virtual(const void* I, const void* T, inf
     TRY(prepare_rank(R[r], static_cast<const uint8_t*>(I) + (size_t)r * bs * d * esz,
                      static_cast<const uint8_t*>(T) + (size_t)r * bs * d * esz, dt, b, d, s, world,
                      static_cast<uint8_t*>(ws) + (size_t)r * per, st));
-    TRY(bwd_begin(R[r], row_lse + (size_t)r * bs, col_lse + (size_t)r * bs, dI + (size_t)r * bs * d,
-                  dT + (size_t)r * bs * d, st));
+    TRY(bwd_begin(R[r], row_lse + (size_t)r * bs, col_lse + (size_t)r * bs, diag + (size_t)r * bs, grad,
+                  dI + (size_t)r * bs * d, st));
   }
   const size_t blk_bytes = (size_t)bs * R[0].L.dk * 2, lse_bytes = (size_t)bs * sizeof(float);
   for (int pass = 0; pass < 2; ++pass) {
@@ -621,7 +622,8 @@ extern "C" infcl_status infcl_backward_virtual(const void* I, const void* T, inf
       held[r] = pass == 0 ? R[r].B : R[r].A;
       held2[r] = R[r].own2(pass == 0 ? 1 : 0);
       if (!R[r].L.f32 && pass == 1)
-        INFCL_CUDA_TRY(cudaMemsetAsync(dT + (size_t)r * bs * d, 0, (size_t)bs * d * sizeof(float), st));
+        diag_init(R[r], 1, dT + (size_t)r * bs * d, diag + (size_t)r * bs, row_lse + (size_t)r * bs,
+                  col_lse + (size_t)r * bs, grad, st);
     }
     for (int k = 0; k < world; ++k) {
       for (int r = 0; r < world; ++r) {
@@ -795,13 +797,13 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[8], 0));
     INFCL_CUDA_TRY(cudaMemcpyAsync(loss_host, lg, sizeof(float), cudaMemcpyDeviceToHost, cout));
     // dI pass (whole), then copy dI out while the dT pass runs chunk by chunk
-    TRY(bwd_begin(R, r, c, dI, dT, st));
+    TRY(bwd_begin(R, r, c, dg, lg + 1, dI, st));
     TRY(bwd_step(R, R.A, R.own2(0), R.B, R.own2(1), true, dI, d, lg + 1, st));
     TRY(pass_end(R, 0, dI, dg, r, c, lg + 1, st));
     INFCL_CUDA_TRY(cudaEventRecord(evs[9], st));
     INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[9], 0));
     INFCL_CUDA_TRY(cudaMemcpyAsync(dI_host, dI, (size_t)b * d * 4, cudaMemcpyDeviceToHost, cout));
-    INFCL_CUDA_TRY(cudaMemsetAsync(dT, 0, (size_t)b * d * 4, st));
+    diag_init(R, 1, dT, dg, r, c, lg + 1, st);
     for (int k = 0; k < nch; ++k) {
       const int r0 = (int)dT_cut[k], r1 = (int)dT_cut[k + 1];
       if (r1 <= r0) continue;

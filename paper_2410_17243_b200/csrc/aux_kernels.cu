@@ -60,28 +60,38 @@ __global__ void merge_rows_kernel(const float2* __restrict__ parts, float2* __re
 }
 
 // Column state j merges the 2P per-CTA slot partials of column j (slots of pairs whose items never touched
-// column j's tile hold stale data and are skipped).  Block = 32 columns x 8 slot groups: group g merges slots
-// g, g+8, ... (independent loads in flight), then the 8 group partials merge in a fixed order (deterministic).
-__global__ void __launch_bounds__(256) merge_cols_kernel(const float2* __restrict__ slots, long long slot_ld,
-                                                         float2* __restrict__ state, int ncols, int n_rb, int n_ct,
-                                                         int P, int all_valid) {
-  __shared__ float2 part[8][32];
+// column j's tile hold stale data and are skipped).  Block = 32 columns x G slot groups: group g merges slots
+// g, g+G, ... (independent loads in flight), then the G group partials merge in a fixed order (deterministic).
+// G = 8 for wide passes (bandwidth-bound); G = 32 for the small blocks of a many-rank ring, where 8 groups left
+// the GPU under-occupied and latency-bound (23 us for 8192 columns).  With no full wave (W = 0) the forward
+// geometry has n_rb < P, so the tail bookkeeping fits 32-bit integers (64-bit kept for rectangular passes).
+template <int G>
+__global__ void __launch_bounds__(32 * G) merge_cols_kernel(const float2* __restrict__ slots, long long slot_ld,
+                                                            float2* __restrict__ state, int ncols, int n_rb,
+                                                            int n_ct, int P, int all_valid) {
+  __shared__ float2 part[G][32];
   const int j = blockIdx.x * 32 + threadIdx.x;
   const int g = threadIdx.y;
   const int W = n_rb / P;
-  const long long T = (long long)(n_rb - W * P) * n_ct;
+  const bool check = !(all_valid || W > 0);
+  const long long T = check ? (long long)n_rb * n_ct : 0;
+  const bool small = T * P < (1LL << 31);  // always for the square forward passes: n_ct <= n_rb < P
   float2 acc = make_float2(-INFINITY, 0.f);
   if (j < ncols) {
     const int ct = j / kColsPerTile;
-    for (int sl = g; sl < 2 * P; sl += 8) {
-      const int p = sl >> 1;
-      bool visited = all_valid || W > 0;
-      if (!visited) {
-        const long long a = tail_begin(T, P, p), e = tail_begin(T, P, p + 1);
-        if (e - a >= n_ct) visited = true;
-        else if (e > a) visited = a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e;
+    for (int sl = g; sl < 2 * P; sl += G) {
+      bool visited = true;
+      if (check) {
+        const int p = sl >> 1;
+        if (small) {
+          const int a = p * (int)T / P, e = (p + 1) * (int)T / P;
+          visited = (e - a >= n_ct) || (e > a && a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e);
+        } else {
+          const long long a = tail_begin(T, P, p), e = tail_begin(T, P, p + 1);
+          visited = (e - a >= n_ct) || (e > a && a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e);
+        }
       }
-      if (visited) acc = merge_ms(acc, slots[(long long)sl * slot_ld + j]);
+      if (visited) acc = merge_ms(acc, __ldg(slots + (long long)sl * slot_ld + j));
     }
   }
   part[g][threadIdx.x] = acc;
@@ -89,7 +99,7 @@ __global__ void __launch_bounds__(256) merge_cols_kernel(const float2* __restric
   if (g == 0 && j < ncols) {
     float2 a = state[j];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a = merge_ms(a, part[k][threadIdx.x]);
+    for (int k = 0; k < G; ++k) a = merge_ms(a, part[k][threadIdx.x]);
     state[j] = a;
   }
 }
@@ -130,19 +140,36 @@ __global__ void scale_log2_kernel(const float* __restrict__ x, float* __restrict
 }
 
 // dA_i += s * g/(2b) * (e^{x_ii - r_i} + e^{x_ii - c_i} - 2) * B_i   (exact fp32 diagonal term, H7)
-__global__ void diag_correction_kernel(float* __restrict__ dA, int ld_dA, const void* __restrict__ B, int ldB,
-                                       int b_f32, const float* __restrict__ diag, const float* __restrict__ r,
-                                       const float* __restrict__ c, const float* __restrict__ grad, float coef_base,
-                                       int n, int d) {
-  const int i = blockIdx.x;
+// exact fp32 diagonal term of Eq.7 (reading H7): dA_i (+)= coef * g * (P_ii + Q_ii - 2) * B_i.  One warp per row,
+// 16-byte stores (d % 8 == 0 and ld % 8 == 0 keep every row 32-B aligned).  init = 1 writes the term (the
+// backward's accumulator initialisation, replacing a memset and a later read-modify-write); init = 0 adds it.
+__global__ void diag_term_kernel(float* __restrict__ dA, int ld_dA, const void* __restrict__ B, int ldB, int b_f32,
+                                 const float* __restrict__ diag, const float* __restrict__ r,
+                                 const float* __restrict__ c, const float* __restrict__ grad, float coef_base, int n,
+                                 int d, int init) {
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= n) return;
+  const int lane = threadIdx.x & 31;
   const float x = diag[i];
-  const float w = coef_base * grad[0] * (expf(x - r[i]) + expf(x - c[i]) - 2.f);
-  for (int k = threadIdx.x; k < d; k += blockDim.x) {
-    float bv;
-    if (b_f32) bv = reinterpret_cast<const float*>(B)[(long long)i * ldB + k];
-    else bv = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(B)[(long long)i * ldB + k]);
-    dA[(long long)i * ld_dA + k] += w * bv;
+  float w = coef_base * grad[0] * (expf(x - r[i]) + expf(x - c[i]) - 2.f);
+  if (INFCL_MUTATION == 4) w = 0.f;
+  float4* out = reinterpret_cast<float4*>(dA + (long long)i * ld_dA);
+  for (int k4 = lane; k4 < (d >> 2); k4 += 32) {
+    float4 bv;
+    if (b_f32) {
+      bv = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(B) + (long long)i * ldB)[k4];
+    } else {
+      const uint2 raw = reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(B) + (long long)i * ldB)[k4];
+      const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+      const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+      bv = make_float4(lo.x, lo.y, hi.x, hi.y);
+    }
+    float4 o = init ? make_float4(0.f, 0.f, 0.f, 0.f) : out[k4];
+    o.x += w * bv.x;
+    o.y += w * bv.y;
+    o.z += w * bv.z;
+    o.w += w * bv.w;
+    out[k4] = o;
   }
 }
 
@@ -209,8 +236,12 @@ void launch_merge_rows(const float2* parts, float2* state, int nrows, const Pass
 }
 void launch_merge_cols(const float2* slots, long long slot_ld, float2* state, int ncols, const PassGeom& g,
                        cudaStream_t s, bool all_valid) {
-  merge_cols_kernel<<<nblk(ncols, 32), dim3(32, 8), 0, s>>>(slots, slot_ld, state, ncols, g.n_rb, g.n_ct, g.npairs,
-                                                            all_valid ? 1 : 0);
+  if (ncols >= 32768)
+    merge_cols_kernel<8><<<nblk(ncols, 32), dim3(32, 8), 0, s>>>(slots, slot_ld, state, ncols, g.n_rb, g.n_ct,
+                                                                 g.npairs, all_valid ? 1 : 0);
+  else
+    merge_cols_kernel<32><<<nblk(ncols, 32), dim3(32, 32), 0, s>>>(slots, slot_ld, state, ncols, g.n_rb, g.n_ct,
+                                                                   g.npairs, all_valid ? 1 : 0);
   ++launch_counter();
 }
 void launch_finalize_lse(const float2* st, float* lse, float* lse2, int n, cudaStream_t s) {
@@ -233,11 +264,11 @@ void launch_scale_log2(const float* x, float* y, int n, cudaStream_t s) {
   scale_log2_kernel<<<nblk(n, 256), 256, 0, s>>>(x, y, n);
   ++launch_counter();
 }
-void launch_diag_correction(float* dA, int ld_dA, const void* B, int ldB, int dtype_f32, const float* diag,
-                            const float* r, const float* c, const float* grad, float coef_base, float /*scale*/, int n,
-                            int d, cudaStream_t s) {
+void launch_diag_term(float* dA, int ld_dA, const void* B, int ldB, int dtype_f32, const float* diag, const float* r,
+                      const float* c, const float* grad, float coef_base, int n, int d, bool init, cudaStream_t s) {
   if (n <= 0) return;
-  diag_correction_kernel<<<n, 256, 0, s>>>(dA, ld_dA, B, ldB, dtype_f32, diag, r, c, grad, coef_base, n, d);
+  diag_term_kernel<<<nblk(n, 8), 256, 0, s>>>(dA, ld_dA, B, ldB, dtype_f32, diag, r, c, grad, coef_base, n, d,
+                                              init ? 1 : 0);
   ++launch_counter();
 }
 void launch_split_f32(const float* x, void* out, int n, int d, int mode, cudaStream_t s) {

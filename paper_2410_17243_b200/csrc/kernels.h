@@ -72,9 +72,9 @@ void launch_loss_partial(const float* r, const float* c, const float* diag, int 
 void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s);
 void launch_scale_log2(const float* x, float* y, int n, cudaStream_t s);
 void launch_set_scalar(float* dst, float v, cudaStream_t s);
-void launch_diag_correction(float* dA, int ld_dA, const void* B, int ldB, int dtype_f32, const float* diag,
-                            const float* r, const float* c, const float* grad, float coef_base, float scale, int n,
-                            int d, cudaStream_t s);
+// exact diagonal gradient term; init = true writes it (accumulator initialisation), false adds it
+void launch_diag_term(float* dA, int ld_dA, const void* B, int ldB, int dtype_f32, const float* diag, const float* r,
+                      const float* c, const float* grad, float coef_base, int n, int d, bool init, cudaStream_t s);
 void launch_split_f32(const float* x, void* out_bf16, int n, int d, int mode, cudaStream_t s);
 void launch_grad_scale(const void* I, int i_f32, const float* dI, long long n, double inv_s, double* out,
                        cudaStream_t s);

@@ -635,3 +635,79 @@ extern "C" int infcl_diag_tma_rate2(const void* X, int nrows, int d, int mode, i
                                                          nrows, mode, ns, iters, out);
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : -3;
 }
+
+// ------------------------------------------------------------------ TMA path probe 3 (diagnostic)
+// Is the ~75 B/clk per-SM streaming cap an SM-ingress limit or an L2-egress limit?  Clusters of 2 CTAs stream
+// 32-KB stages (two 2D SW128 boxes of [64 x 128 rows]).  mode 0: each CTA loads both boxes itself; mode 1: CTA r
+// loads box r with .multicast::cluster to both CTAs (each SM still receives 32 KB per stage, L2 sends half).
+// The peer's consumer must free a stage before it is refilled, so `empty` takes one arrival from each CTA.
+namespace infcl {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64, 1)
+    probe_tma3_kernel(const __grid_constant__ CUtensorMap tb, int nrows, int mode, int ns, int iters,
+                      long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[8], empty[8];
+  const uint32_t cta = cluster_ctarank();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ns; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], mode == 1 ? 2 : 1);
+    }
+    fence_mbar_init();
+  }
+  cluster_sync();
+  const long long t0 = clock64();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    uint32_t ph = 0;
+    int row = ((blockIdx.x >> (mode == 1 ? 1 : 0)) * 997) % (nrows - 256);
+    for (int i = 0; i < iters; ++i) {
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_arrive_expect_tx(&full[s], 32768);
+      uint8_t* dst = smem_raw + s * 32768;
+      const int col = (i & 7) * 64;
+      if (mode == 0) {
+        tma_load_2d(dst, &tb, &full[s], col, row);
+        tma_load_2d(dst + 16384, &tb, &full[s], col, row + 128);
+      } else {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
+            "[%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst + cta * 16384)),
+            "l"(reinterpret_cast<uint64_t>(&tb)), "r"(smem_u32(&full[s])), "r"(col), "r"(row + (int)cta * 128),
+            "h"((uint16_t)0x3)
+            : "memory");
+      }
+      row += 256;
+      if (row >= nrows - 256) row -= nrows - 512;
+      if (++s == ns) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (threadIdx.x == 32) {
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < iters; ++i) {
+      mbar_wait(&full[s], ph);
+      mbar_arrive(&empty[s]);
+      if (mode == 1) mbar_arrive_cluster(&empty[s], cta ^ 1u);
+      if (++s == ns) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    out[blockIdx.x] = clock64() - t0;
+  }
+  cluster_sync();
+}
+}  // namespace infcl
+
+extern "C" int infcl_diag_tma_rate3(const void* X, int nrows, int d, int mode, int ns, int iters, int nblocks,
+                                    long long* out) {
+  CUtensorMap b;
+  if (make_tmap_bf16(&b, X, nrows, d, d, 64, 128)) return -1;
+  if (ns < 1 || ns > 6 || (nblocks & 1)) return -2;
+  cudaFuncSetAttribute(infcl::probe_tma3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 32768);
+  infcl::probe_tma3_kernel<<<nblocks, 64, 6 * 32768>>>(b, nrows, mode, ns, iters, out);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : -3;
+}
