@@ -6,11 +6,12 @@
 // scripts/experiments/walk_probe4.py) show those run at 70-78 % of the tensor rate once the ring handshakes are in the
 // loop, while M=256 pair MMAs (128 cycles each) stay at 100 % with the same handshakes.  The forward has no
 // TMEM-resident accumulator besides S, so it can afford 256-row pair tiles: S (256 x 256) = A_R * B_C^T with
-// tcgen05.mma.cta_group::2 M=256 N=256 (per SM: 128 rows x 256 columns, TMEM lane = row).  The stationary
-// rows are NOT kept resident (128 rows x d bf16 would leave too little smem for the ring): every ring stage
-// carries one 64-wide K block of A (128 rows, 16 KB) and of B (128 columns, 16 KB) per SM, the A block coming
-// from L2 after the first column tile of the segment.  Per-SM operand traffic per MMA cycle is the same as the
-// narrow kernel's (64 B/clk at full rate) but 6 stages (192 KB) are in flight instead of 4.
+// tcgen05.mma.cta_group::2 M=256 N=256 (per SM: 128 rows x 256 columns, TMEM lane = row).  At d <= 512 the
+// segment's stationary rows are resident (128 rows x d bf16 = up to 128 KB per SM) and each ring stage carries
+// one 64-wide K block of B only (16 KB; 5 stages): 32 B/clk of L2->SM operand traffic at the full tensor rate.
+// At d = 768 A cannot be resident next to a useful ring, so every 32-KB stage carries one K block of A
+// (128 rows) and of B (128 columns) per SM, A coming from L2 after the segment's first tile (64 B/clk, the
+// narrow kernel's figure, with 6 stages = 192 KB in flight).
 //
 // Epilogue: 8 warps; warp (q = warp % 4, u = warp / 4) owns rows 32q..32q+31 (its TMEM lane quarter) and
 // columns 128u..128u+127 of the tile, processed as two 64-column chunks with the narrow kernel's per-chunk
@@ -34,13 +35,20 @@ constexpr int kWRows = 256;       // stationary rows per CTA pair (128 per SM)
 constexpr int kWStage = 32768;    // ring stage per SM: A block 16 KB + B block 16 KB (one 64-wide K step)
 constexpr int kWBufCols = 256;    // TMEM columns per S buffer
 
-template <bool DBG>
+template <bool DBG, bool RESA>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     wide_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ KParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];  // SW128 operands need 1024-B alignment
   if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u)) __trap();
-  uint8_t* sStage = smem_raw;
+  // RESA (A resident, d <= 512): the segment's 128 stationary rows per SM live in smem (KB x 16-KB K blocks)
+  // and the ring stages carry only B (16 KB), halving the L2->SM operand bytes per MMA; the first tile of a
+  // segment brings A block kb inside ring stage kb's transaction.  Safe to overwrite: the previous reader of
+  // A block kb is the MMA KB ring uses earlier, and the producer's empty wait for this use guarantees every MMA
+  // up to n_stages uses earlier has completed (the host keeps n_stages <= KB).
+  uint8_t* sA = smem_raw;
+  uint8_t* sStage = smem_raw + (RESA ? p.KB * kBoxB : 0);
+  constexpr int kStg = RESA ? kBoxB : kWStage;
 
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], sfull[2], sfree[2];
   __shared__ uint32_t tmem_base;
@@ -85,19 +93,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       while (it < nk) {
         int rb, ct0;
         S.decode(it, rb, ct0);
-        const long long seg_end = S.seg_end(it);
+        const long long seg_end = S.seg_end(it), seg_start = it;
         const int a_row = rb * kWRows + (int)cta * 128;
         for (int ct = ct0; it < seg_end; ++it, ++ct) {  // a segment's column tiles are consecutive
           const int b_row = (ct + (INFCL_MUTATION == 3 && ct == 0 ? 1 : 0)) * kColsPerTile + (int)cta * 128;
+          const bool lda = !RESA || it == seg_start;  // this tile's stages bring A blocks
           for (int kb = 0; kb < p.KB; ++kb) {
             ring_acquire(wc, empty, stage, ph, p.pair_commit);
             if (DBG && p.notma) {
               if (cta == 0) mbar_arrive(&full[stage]);
             } else {
-              if (cta == 0) mbar_arrive_expect_tx(&full[stage], 2 * kWStage);
-              uint8_t* dst = sStage + stage * kWStage;
-              tma_load_2d_pair(dst, &tmA, &full[stage], kb * 64, a_row);
-              tma_load_2d_pair(dst + kBoxB, &tmB, &full[stage], kb * 64, b_row);
+              if (cta == 0) mbar_arrive_expect_tx(&full[stage], (lda ? 4 : 2) * kBoxB);
+              uint8_t* dst = sStage + stage * kStg;
+              if (lda) tma_load_2d_pair(RESA ? sA + kb * kBoxB : dst, &tmA, &full[stage], kb * 64, a_row);
+              tma_load_2d_pair(RESA ? dst : dst + kBoxB, &tmB, &full[stage], kb * 64, b_row);
             }
             if (++stage == p.n_stages) {
               stage = 0;
@@ -126,9 +135,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           wc.wait(&full[stage], ph, 5);
           const unsigned long long t_is = DBG ? clock64() : 0ull;
           tc_fence_after();
-          const uint32_t st = smem_u32(sStage + stage * kWStage);
-          umma_stage_pair<false, 0, 0>(dS, (uint32_t)smem_desc_sw128(st, 16, 1024),
-                                       (uint32_t)smem_desc_sw128(st + kBoxB, 16, 1024), idS, kb != 0);
+          const uint32_t st = smem_u32(sStage + stage * kStg);
+          const uint32_t sa = RESA ? smem_u32(sA + kb * kBoxB) : st;
+          umma_stage_pair<false, 0, 0>(dS, (uint32_t)smem_desc_sw128(sa, 16, 1024),
+                                       (uint32_t)smem_desc_sw128(RESA ? st : st + kBoxB, 16, 1024), idS, kb != 0);
           ring_release(empty, stage, p.pair_commit);
           if (DBG) wc.acc[11] += clock64() - t_is;
           if (++stage == p.n_stages) {
@@ -282,22 +292,30 @@ infcl_status launch_wide_forward(const PassArgs& a, cudaStream_t s) {
   static int static_smem = -1;
   if (static_smem < 0) {
     cudaFuncAttributes fa;
-    INFCL_CUDA_TRY(cudaFuncGetAttributes(&fa, wide_fwd_kernel<false>));
+    INFCL_CUDA_TRY(cudaFuncGetAttributes(&fa, wide_fwd_kernel<false, false>));
     static_smem = (int)fa.sharedSizeBytes;
   }
   const long long budget = 232448 - ((static_smem + 1023) / 1024) * 1024;
-  int ns = (int)std::min<long long>(kMaxStages, budget / kWStage);
+  // A resident when it leaves >= 4 B-only stages (KB <= 8, i.e. d <= 512) and KB >= 4; n_stages <= KB keeps
+  // the A-block overwrite safe (see the kernel).  INFCL_FWD_STREAM_A=1: A/B switch back to streamed A.
+  const char* sa_env = getenv("INFCL_FWD_STREAM_A");
+  const bool resa = !(sa_env && *sa_env && *sa_env != '0') && k.KB >= 4 &&
+                    budget - (long long)k.KB * kBoxB >= 4LL * kBoxB;
+  const long long stage_bytes = resa ? kBoxB : kWStage;
+  int ns = (int)std::min<long long>(kMaxStages, (budget - (resa ? (long long)k.KB * kBoxB : 0)) / stage_bytes);
+  if (resa) ns = std::min(ns, k.KB);
   if (const char* e = getenv("INFCL_STAGES")) ns = std::max(2, std::min(ns, atoi(e)));
   k.n_stages = ns;
   k.pair_commit = (ns % 2 == 0 && !getenv("INFCL_NO_PAIR_COMMIT")) ? 1 : 0;
-  const size_t smem = (size_t)ns * kWStage;
+  const size_t smem = (size_t)ns * stage_bytes + (resa ? (size_t)k.KB * kBoxB : 0);
   CUtensorMap tmA, tmB;
   infcl_status st = make_tmap_bf16(&tmA, a.A, a.nrows, a.dk, a.ld, 64, 128);
   if (st) return st;
   if ((st = make_tmap_bf16(&tmB, a.B, a.ncols, a.dk, a.ld, 64, 128))) return st;
   k.noepi = getenv("INFCL_DEBUG_NOEPI") != nullptr;
   k.notma = getenv("INFCL_DEBUG_NOTMA") != nullptr;
-  auto kern = dbg ? wide_fwd_kernel<true> : wide_fwd_kernel<false>;
+  auto kern = resa ? (dbg ? wide_fwd_kernel<true, true> : wide_fwd_kernel<false, true>)
+                  : (dbg ? wide_fwd_kernel<true, false> : wide_fwd_kernel<false, false>);
   INFCL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0 = profile_begin(s);
   kern<<<dim3(2 * g.npairs), dim3(kThreads), smem, s>>>(tmA, tmB, k);

@@ -125,12 +125,12 @@ def test_e2e_host_entry_chunked(b, d):
     assert rel_norm(dT.numpy()[rows], rdT) <= 2e-3
 
 
-@pytest.mark.parametrize("b", [256 * 74 + 300, 256 * 74 * 2 + 4000])
-def test_wide_forward_waves_and_tail(b):
+@pytest.mark.parametrize("b,d", [(256 * 74 + 300, 64), (256 * 74 * 2 + 4000, 64), (256 * 74 + 300, 512)])
+def test_wide_forward_waves_and_tail(b, d):
     """Row counts that give the wide forward (256 rows per pair) one / two full waves of 74 pairs plus a ragged
     tail split across pairs (Sched tail ranges, row-partial tail slots): every r_j, c_j and the loss exact
-    against the streamed fp64 oracle, plus the backward's sampled gradient rows."""
-    d = 64
+    against the streamed fp64 oracle, plus the backward's sampled gradient rows.  d = 512 runs the resident-A
+    variant (segment changes reload the stationary rows inside the ring transactions); d = 64 streams A."""
     I, T = make_features(b, d, seed=23, dist="paired")
     Id, Td = I.cuda(), T.cuda()
     loss, r, c, dg = K.infcl_forward(Id, Td, b, S)

@@ -247,3 +247,12 @@ def test_parity_narrow_forward_kernel(b, d, monkeypatch):
     monkeypatch.setenv("INFCL_FWD_NARROW", "1")
     I, T = make_features(b, d, seed=21, dist="paired")
     check_all(I, T, 14.2857)
+
+
+@pytest.mark.parametrize("b,d", [(4096, 512), (5000, 384)])
+def test_parity_wide_forward_streamed_a(b, d, monkeypatch):
+    """The wide forward with streamed A (the d = 768 layout) stays parity-green at d <= 512, where the default
+    keeps the stationary rows resident (INFCL_FWD_STREAM_A=1 switches back)."""
+    monkeypatch.setenv("INFCL_FWD_STREAM_A", "1")
+    I, T = make_features(b, d, seed=22, dist="paired")
+    check_all(I, T, 14.2857, want_grads=False)
