@@ -77,19 +77,19 @@ __global__ void __launch_bounds__(32 * G) merge_cols_kernel(const float2* __rest
   const long long T = check ? (long long)n_rb * n_ct : 0;
   const bool small = T * P < (1LL << 31);  // always for the square forward passes: n_ct <= n_rb < P
   float2 acc = make_float2(-INFINITY, 0.f);
-  if (j < ncols) {
+  if (j < ncols && !check) {  // every slot holds data: unconditional loads
+    for (int sl = g; sl < 2 * P; sl += G) acc = merge_ms(acc, __ldg(slots + (long long)sl * slot_ld + j));
+  } else if (j < ncols) {
     const int ct = j / kColsPerTile;
     for (int sl = g; sl < 2 * P; sl += G) {
-      bool visited = true;
-      if (check) {
-        const int p = sl >> 1;
-        if (small) {
-          const int a = p * (int)T / P, e = (p + 1) * (int)T / P;
-          visited = (e - a >= n_ct) || (e > a && a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e);
-        } else {
-          const long long a = tail_begin(T, P, p), e = tail_begin(T, P, p + 1);
-          visited = (e - a >= n_ct) || (e > a && a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e);
-        }
+      const int p = sl >> 1;
+      bool visited;
+      if (small) {
+        const int a = p * (int)T / P, e = (p + 1) * (int)T / P;
+        visited = (e - a >= n_ct) || (e > a && a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e);
+      } else {
+        const long long a = tail_begin(T, P, p), e = tail_begin(T, P, p + 1);
+        visited = (e - a >= n_ct) || (e > a && a + ((ct - a % n_ct) % n_ct + n_ct) % n_ct < e);
       }
       if (visited) acc = merge_ms(acc, __ldg(slots + (long long)sl * slot_ld + j));
     }
