@@ -1,11 +1,12 @@
-"""Tiny forward+backward for compute-sanitizer runs: both forward kernels, the backward,
+"""Tiny forward+backward for compute-sanitizer runs: both forward kernels (wide: streamed and
+resident A), the backward,
 the virtual ring and the host e2e entry on small shapes with ragged tails."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2410_17243_b200 import loss as K
 from synth import make_features
-for b, d in ((300, 64), (520, 128)):
+for b, d in ((300, 64), (520, 128), (600, 256), (1100, 512)):  # d >= 256: resident-A forward
     I, T = make_features(b, d, seed=1, dist="paired")
     Id, Td = I.cuda(), T.cuda()
     loss, r, c, dg = K.infcl_forward(Id, Td, b, 14.2857)
