@@ -205,22 +205,30 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # INFCL_BENCH_SAME_GPU=1 (test only): every rank on cuda:0 with a gloo process group, to exercise the N>1
+    # path (IPC transport, timing reduction, JSON line) on a one-GPU box; its numbers are not throughput
+    same_gpu = os.environ.get("INFCL_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N>1 must be launched with torchrun (one rank per GPU)")
     torch.cuda.set_device(local)
     comm = None
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        comm = K.RingComm()
     b, d, name = workload(args, world)
     if b % world:
         raise SystemExit(f"b={b} not divisible by world={world}")
+    if world > 1:
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = K.RingComm(transport=args.transport, max_b=b, max_d=d)
     bs = b // world
     s = args.scale
     dev = torch.device("cuda", local)
     I, T = make_features_device(bs, d, seed=args.seed * 1000 + rank, device=dev)
-    ws = K.alloc_workspace(b, d, world, torch.bfloat16, dev)
+    ws = K.alloc_workspace(b, d, world, torch.bfloat16, dev, comm=comm)
     g = torch.ones((), device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
@@ -267,7 +275,8 @@ def run_ours(args):
     ms_step = max_over_ranks(fwd_ms + bwd_ms)
     fwd_ms = max_over_ranks(fwd_ms)
     bwd_ms = max_over_ranks(bwd_ms)
-    peak_gb = max_over_ranks(torch.cuda.max_memory_allocated(dev) / 1e9)
+    # torch-allocated peak plus the one device region the library owns (the IPC transport's receive slots)
+    peak_gb = max_over_ranks((torch.cuda.max_memory_allocated(dev) + (comm.region_bytes() if comm else 0)) / 1e9)
     value = b / (ms_step / 1e3)
     lval = float(loss.item())
 
@@ -303,7 +312,7 @@ def run_ours(args):
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-               "config": {"workload": name, "b": b, "d": d, "logit_scale": s, "parallelism": f"ring{world}",
+               "config": {"workload": name, "b": b, "d": d, "logit_scale": s, "parallelism": f"ring{world}" + (f"-{args.transport}" if world > 1 else ""),
                           "l2": "512 MB buffer written between timed steps (outside per-step events)",
                           "inputs": "L2-normalised N(0,1) rows, bf16 RNE, generated on device"},
                "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "peak_gb_per_gpu": peak_gb, "loss": lval,
@@ -337,7 +346,7 @@ def run_e2e(args, K, b, d, bs, s, rank, world, comm, dev):
             K.infcl_loss_grad_host(Ih, Th, s, 1.0, scratch, out)
             times.append(time.perf_counter() - t0)
     else:
-        ws = K.alloc_workspace(b, d, world, torch.bfloat16, dev)
+        ws = K.alloc_workspace(b, d, world, torch.bfloat16, dev, comm=comm)
         g = torch.ones((), device=dev)
         dIh = torch.empty(bs, d, dtype=torch.float32).pin_memory()
         dTh = torch.empty_like(dIh)
@@ -373,6 +382,8 @@ def main(argv=None):
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", choices=["ipc", "nccl"], default="ipc",
+                    help="ring transport for N>1: copy-engine writes over CUDA IPC peer memory (default) or NCCL P2P")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         run_reference(args)

@@ -50,8 +50,15 @@ typedef enum {
 
 typedef enum { INFCL_BF16 = 0, INFCL_FP32 = 1 } infcl_dtype;
 
-/* Opaque ring communicator: owns an ncclComm_t, a communication stream and events.  NULL for world==1. */
+/* Opaque ring communicator: a transport, a communication stream and events.  NULL for world==1. */
 typedef struct infcl_comm_s* infcl_comm;
+
+/* Ring transports.  NCCL: grouped ncclSend/ncclRecv (the receive buffers are in the caller's workspace).
+ * IPC: one-sided copy-engine writes into the peer's library-owned receive region over CUDA IPC mappings
+ * (NVLink/NVSwitch peer memory across GPUs; also valid when several ranks share one GPU), synchronised by
+ * stream memory operations on 32-bit fill/release counters -- the exchange uses no SM, so it overlaps the
+ * persistent compute kernels that occupy every SM. */
+typedef enum { INFCL_TRANSPORT_NCCL = 0, INFCL_TRANSPORT_IPC = 1 } infcl_transport;
 
 const char* infcl_status_string(infcl_status s);
 /* Thread-local detail of the last failing call on this thread (e.g. "b=7 not divisible by world=2"). */
@@ -69,8 +76,29 @@ infcl_status infcl_get_unique_id(void* id128);
 infcl_status infcl_comm_init(infcl_comm* out, int rank, int world, const void* id128, int device);
 infcl_status infcl_comm_destroy(infcl_comm comm);
 
-/* Bytes of device workspace infcl_forward/infcl_backward need for this configuration (0 on bad args). */
+/* IPC transport (the same ring schedule, Q13/Q14/Q15 readings; P:216-219 overlap):
+ * infcl_comm_init_ipc: allocates and zeroes this rank's receive region on `device` (2 slots each of one
+ *   travelling block [max_b/world][d'] bf16 (d' = 3 max_d for fp32 inputs), one column state and one LSE vector,
+ *   plus a 4-KB counter page; infcl_comm_ipc_region_bytes reports its size).  The region is the one device
+ *   allocation the library owns; it is freed by infcl_comm_destroy.  2 <= world <= 64.
+ * infcl_comm_ipc_handle: writes the region's 64-byte cudaIpcMemHandle_t to host memory `handle64`.
+ * infcl_comm_ipc_connect: `handles` = world x 64 bytes (host), rank q's handle at offset 64 q, as gathered
+ *   by the caller (torch.distributed all_gather); maps every peer region.  Must precede the first call.
+ * Errors: INFCL_ERR_UNSUPPORTED without stream memory operations; INFCL_ERR_CUDA on IPC failures;
+ *   INFCL_ERR_WORKSPACE when a call's shard exceeds the region's (max_b, max_d). */
+infcl_status infcl_comm_init_ipc(infcl_comm* out, int rank, int world, int device, int64_t max_b, int max_d,
+                                 infcl_dtype dt);
+infcl_status infcl_comm_ipc_handle(infcl_comm comm, void* handle64);
+infcl_status infcl_comm_ipc_connect(infcl_comm comm, const void* handles);
+size_t infcl_comm_ipc_region_bytes(infcl_comm comm);
+/* INFCL_TRANSPORT_NCCL / INFCL_TRANSPORT_IPC, or -1 for NULL */
+int infcl_comm_transport(infcl_comm comm);
+
+/* Bytes of device workspace infcl_forward/infcl_backward need for this configuration (0 on bad args), for the
+ * NCCL transport (or world == 1).  infcl_comm_workspace_bytes: the same for the transport of `comm` (the IPC
+ * transport receives into its own region, so its workspace holds no ring buffers); comm may be NULL. */
 size_t infcl_workspace_bytes(int64_t b, int d, int world, infcl_dtype dt);
+size_t infcl_comm_workspace_bytes(infcl_comm comm, int64_t b, int d, int world, infcl_dtype dt);
 
 /* ---------------------------------------------------------------------------------------------------
  * infcl_forward -- Alg.1 over Alg.2, plus the symmetric column direction.

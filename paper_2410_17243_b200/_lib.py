@@ -14,6 +14,8 @@ LIB_PATH = os.environ.get("INFCL_LIB") or os.path.join(_HERE, "libinfcl.so")
 
 INFCL_BF16 = 0
 INFCL_FP32 = 1
+INFCL_TRANSPORT_NCCL = 0
+INFCL_TRANSPORT_IPC = 1
 
 STATUS = {0: "INFCL_OK", 1: "INFCL_ERR_INVALID_ARG", 2: "INFCL_ERR_SHAPE", 3: "INFCL_ERR_CONFIG",
           4: "INFCL_ERR_CUDA", 5: "INFCL_ERR_NCCL", 6: "INFCL_ERR_WORKSPACE", 7: "INFCL_ERR_UNSUPPORTED"}
@@ -33,6 +35,12 @@ SIGNATURES = {
     "infcl_comm_init": (_i, [ctypes.POINTER(_p), _i, _i, _p, _i]),
     "infcl_comm_destroy": (_i, [_p]),
     "infcl_workspace_bytes": (_sz, [_i64, _i, _i, _i]),
+    "infcl_comm_workspace_bytes": (_sz, [_p, _i64, _i, _i, _i]),
+    "infcl_comm_init_ipc": (_i, [ctypes.POINTER(_p), _i, _i, _i, _i64, _i, _i]),
+    "infcl_comm_ipc_handle": (_i, [_p, _p]),
+    "infcl_comm_ipc_connect": (_i, [_p, _p]),
+    "infcl_comm_ipc_region_bytes": (_sz, [_p]),
+    "infcl_comm_transport": (_i, [_p]),
     "infcl_forward": (_i, [_p, _p, _p, _i, _i64, _i, _f, _i, _i, _p, _p, _p, _p, _p, _sz, _p]),
     "infcl_backward": (_i, [_p, _p, _p, _i, _i64, _i, _f, _i, _i, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "infcl_forward_virtual": (_i, [_p, _p, _i, _i64, _i, _f, _i, _p, _p, _p, _p, _p, _sz, _p]),

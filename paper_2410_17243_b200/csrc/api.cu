@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -22,6 +23,12 @@
 #include "kernels.h"
 
 using namespace infcl;
+
+#define TRY(x)                      \
+  do {                              \
+    infcl_status _s = (x);          \
+    if (_s != INFCL_OK) return _s;  \
+  } while (0)
 
 // ------------------------------------------------------------------------------------------ NCCL (dlopen)
 namespace {
@@ -76,12 +83,79 @@ NcclApi& nccl() {
   } while (0)
 }  // namespace
 
+// Ring transports (infcl.h): INFCL_TRANSPORT_NCCL -- grouped ncclSend/ncclRecv into the caller's workspace;
+// INFCL_TRANSPORT_IPC -- one-sided copy-engine writes over CUDA IPC peer mappings (NVLink/NVSwitch P2P on a
+// multi-GPU box, same-device mappings when several ranks share one GPU) into a library-owned receive region,
+// synchronised by stream memory operations on 32-bit counters (cuStreamWaitValue32 / cuStreamWriteValue32):
+// no SM is used by the exchange, so it overlaps the persistent pair kernels, which occupy every SM.
+namespace {
+enum XKind { XK_BLK = 0, XK_CS = 1, XK_LSE = 2, XK_N = 3 };  // travelling block, column state, LSE vector
+
+typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct MemOps {
+  PFN_streamValue32 wait = nullptr, write = nullptr;
+  bool ok = false;
+};
+MemOps& memops() {
+  static MemOps m;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      m.wait = reinterpret_cast<PFN_streamValue32>(p);
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      m.write = reinterpret_cast<PFN_streamValue32>(p);
+    m.ok = m.wait && m.write;
+  }
+  return m;
+}
+
+// IPC receive region of one rank (cudaMalloc'ed, exported): a flag page then the receive slots.
+struct IpcFlags {
+  uint32_t ready[XK_N][2];  // written by rank r+1 after filling slot (kind, s): its fill count
+  uint32_t freed[XK_N][2];  // written by rank r-1 after releasing ITS slot (kind, s): its release count
+  uint32_t acc_ready[64];   // written by rank q after depositing its loss partial in acc_in[q]: call count
+  uint32_t acc_done[64];    // written by rank q after it summed the partials of a call: call count
+  double acc_in[64];        // loss partials of every rank (the IPC all-reduce)
+};
+constexpr size_t kFlagBytes = 4096;
+static_assert(sizeof(IpcFlags) <= kFlagBytes, "flag page");
+}  // namespace (transport)
+
 struct infcl_comm_s {
+  int transport = INFCL_TRANSPORT_NCCL;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1, device = 0;
-  cudaStream_t stream = nullptr;  // communication stream (NCCL P2P overlapped with compute)
+  cudaStream_t stream = nullptr;  // communication stream (exchange overlapped with compute)
   std::vector<cudaEvent_t> ev;    // event pool
+  // NCCL transport: per-call receive slots in the caller's workspace and their arrival events
+  void* nslot[XK_N][2] = {};
+  cudaEvent_t evr[XK_N][2] = {};
+  // IPC transport
+  uint8_t* region = nullptr;
+  size_t cap[XK_N] = {}, off[XK_N] = {}, region_bytes = 0;
+  int64_t max_b = 0;
+  int max_d = 0;
+  std::vector<uint8_t*> peers;  // mapped receive regions of every rank (peers[rank] = region)
+  bool connected = false;
+  uint32_t fills[XK_N][2] = {}, rels[XK_N][2] = {}, calls = 0;
 };
+
+namespace {
+infcl_status make_comm_stream(infcl_comm c) {
+  INFCL_CUDA_TRY(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, -1));
+  c->ev.resize(8);
+  for (auto& e : c->ev) INFCL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& row : c->evr)
+    for (auto& e : row) INFCL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return INFCL_OK;
+}
+IpcFlags* flags_of(uint8_t* region) { return reinterpret_cast<IpcFlags*>(region); }
+}  // namespace
 
 extern "C" infcl_status infcl_get_unique_id(void* id128) {
   if (!id128) return fail(INFCL_ERR_INVALID_ARG, "null id buffer");
@@ -108,22 +182,109 @@ extern "C" infcl_status infcl_comm_init(infcl_comm* out, int rank, int world, co
     delete c;
     return fail(INFCL_ERR_NCCL, "ncclCommInitRank failed");
   }
-  cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, -1);
-  c->ev.resize(8);
-  for (auto& e : c->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (infcl_status st = make_comm_stream(c)) {
+    infcl_comm_destroy(c);
+    return st;
+  }
   *out = c;
   return INFCL_OK;
 }
 
 extern "C" infcl_status infcl_comm_destroy(infcl_comm c) {
   if (!c) return INFCL_OK;
+  cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto e : c->ev) cudaEventDestroy(e);
+  for (auto& row : c->evr)
+    for (auto e : row)
+      if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->comm) nccl().CommDestroy(c->comm);
+  for (int q = 0; q < (int)c->peers.size(); ++q)
+    if (q != c->rank && c->peers[q]) cudaIpcCloseMemHandle(c->peers[q]);
+  if (c->region) cudaFree(c->region);
   delete c;
   return INFCL_OK;
 }
+
+// ---- IPC transport setup: create (allocate + zero the receive region), export, connect (map every peer)
+extern "C" infcl_status infcl_comm_init_ipc(infcl_comm* out, int rank, int world, int device, int64_t max_b,
+                                            int max_d, infcl_dtype dt) {
+  if (!out) return fail(INFCL_ERR_INVALID_ARG, "null argument");
+  if (world < 2 || world > 64 || rank < 0 || rank >= world)
+    return fail(INFCL_ERR_CONFIG, "IPC ring needs 2 <= world <= 64 and 0 <= rank < world");
+  if (max_b < world || max_d < 8 || max_b % world) return fail(INFCL_ERR_SHAPE, "bad max_b / max_d");
+  if (!memops().ok) return fail(INFCL_ERR_UNSUPPORTED, "cuStreamWaitValue32/cuStreamWriteValue32 unavailable");
+  INFCL_CUDA_TRY(cudaSetDevice(device));
+  auto* c = new infcl_comm_s();
+  c->transport = INFCL_TRANSPORT_IPC;
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  c->max_b = max_b;
+  c->max_d = max_d;
+  const size_t bs = (size_t)(max_b / world), dk = dt == INFCL_FP32 ? 3 * (size_t)max_d : (size_t)max_d;
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  c->cap[XK_BLK] = al(bs * dk * 2);
+  c->cap[XK_CS] = al(bs * sizeof(float2));
+  c->cap[XK_LSE] = al(bs * sizeof(float));
+  size_t o = kFlagBytes;
+  for (int k = 0; k < XK_N; ++k) {
+    c->off[k] = o;
+    o += 2 * c->cap[k];
+  }
+  c->region_bytes = o;
+  cudaError_t e = cudaMalloc(&c->region, o);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(INFCL_ERR_CUDA, std::string("IPC region cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  if ((e = cudaMemset(c->region, 0, kFlagBytes)) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
+    infcl_comm_destroy(c);
+    return fail(INFCL_ERR_CUDA, std::string("IPC region init: ") + cudaGetErrorString(e));
+  }
+  if (infcl_status st = make_comm_stream(c)) {
+    infcl_comm_destroy(c);
+    return st;
+  }
+  *out = c;
+  return INFCL_OK;
+}
+
+extern "C" infcl_status infcl_comm_ipc_handle(infcl_comm c, void* handle64) {
+  if (!c || !handle64 || c->transport != INFCL_TRANSPORT_IPC) return fail(INFCL_ERR_INVALID_ARG, "not an IPC comm");
+  cudaIpcMemHandle_t h;
+  INFCL_CUDA_TRY(cudaSetDevice(c->device));
+  INFCL_CUDA_TRY(cudaIpcGetMemHandle(&h, c->region));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle64, &h, sizeof(h));
+  return INFCL_OK;
+}
+
+extern "C" infcl_status infcl_comm_ipc_connect(infcl_comm c, const void* handles) {
+  if (!c || !handles || c->transport != INFCL_TRANSPORT_IPC) return fail(INFCL_ERR_INVALID_ARG, "not an IPC comm");
+  if (c->connected) return INFCL_OK;
+  INFCL_CUDA_TRY(cudaSetDevice(c->device));
+  c->peers.assign(c->world, nullptr);
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) {
+      c->peers[q] = c->region;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const uint8_t*>(handles) + 64 * (size_t)q, sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(INFCL_ERR_CUDA, "cudaIpcOpenMemHandle(rank " + std::to_string(q) + "): " +
+                                                          cudaGetErrorString(e));
+    c->peers[q] = static_cast<uint8_t*>(p);
+  }
+  c->connected = true;
+  return INFCL_OK;
+}
+
+extern "C" int infcl_comm_transport(infcl_comm c) { return c ? c->transport : -1; }
+extern "C" size_t infcl_comm_ipc_region_bytes(infcl_comm c) { return c ? c->region_bytes : 0; }
 
 // ------------------------------------------------------------------------------------------ workspace
 namespace {
@@ -139,7 +300,9 @@ struct Layout {
       off_dscr, off_acc, total;
 };
 
-Layout make_layout(int64_t b, int d, int world, infcl_dtype dt) {
+// ring_ws: the ring's receive buffers live in the workspace (NCCL transport); the IPC transport receives
+// into its own exported region, so its workspace has none
+Layout make_layout(int64_t b, int d, int world, infcl_dtype dt, bool ring_ws = true) {
   Layout L;
   L.bs = (int)(b / world);
   L.d = d;
@@ -162,8 +325,8 @@ Layout make_layout(int64_t b, int d, int world, infcl_dtype dt) {
   L.off_rstate = take((size_t)L.bs * sizeof(float2));
   L.off_cstate = take((size_t)3 * L.bs * sizeof(float2));
   L.off_own2 = take((size_t)2 * L.bs * sizeof(float));
-  L.off_ring_lse = take(world > 1 ? (size_t)2 * L.bs * sizeof(float) : 0);
-  L.off_ring_blk = take(world > 1 ? (size_t)2 * L.bs * L.dk * 2 : 0);
+  L.off_ring_lse = take(world > 1 && ring_ws ? (size_t)2 * L.bs * sizeof(float) : 0);
+  L.off_ring_blk = take(world > 1 && ring_ws ? (size_t)2 * L.bs * L.dk * 2 : 0);
   L.off_expA = take(L.f32 ? (size_t)L.bs * L.dk * 2 : 0);
   L.off_expB = take(L.f32 ? (size_t)L.bs * L.dk * 2 : 0);
   L.off_dscr = take(L.f32 ? (size_t)L.bs * L.dk * sizeof(float) : 0);
@@ -220,8 +383,8 @@ struct Rank {
 };
 
 infcl_status prepare_rank(Rank& R, const void* I, const void* T, infcl_dtype dt, int64_t b, int d, float s, int world,
-                          void* ws, cudaStream_t st) {
-  R.L = make_layout(b, d, world, dt);
+                          void* ws, cudaStream_t st, bool ring_ws = true) {
+  R.L = make_layout(b, d, world, dt, ring_ws);
   R.ws = static_cast<uint8_t*>(ws);
   R.s = s;
   R.b = b;
@@ -398,13 +561,88 @@ cudaEvent_t ev(infcl_comm c, int i) { return c->ev[i % c->ev.size()]; }
 int prev_rank(int r, int n) { return (r - 1 + n) % n; }
 int next_rank(int r, int n) { return (r + 1) % n; }
 
-// grouped send(to r-1) / recv(from r+1) of one buffer pair on the comm stream
-infcl_status ring_exchange(infcl_comm c, const void* send, void* recv, size_t bytes) {
+// ---- ring exchange primitives (both transports); every rank runs the same schedule, so the k-th send of
+// (kind, s) by rank r and the k-th fill of r's own slot (kind, s) by rank r+1 pair up.
+// slot(kind, s): where the block received in slot s lives (NCCL: the caller's workspace; IPC: own region)
+void* xslot(infcl_comm c, int kind, int s) {
+  return c->transport == INFCL_TRANSPORT_IPC ? c->region + c->off[kind] + (size_t)s * c->cap[kind] : c->nslot[kind][s];
+}
+size_t off_ready(int kind, int s) { return offsetof(IpcFlags, ready) + (size_t)(2 * kind + s) * 4; }
+size_t off_freed(int kind, int s) { return offsetof(IpcFlags, freed) + (size_t)(2 * kind + s) * 4; }
+size_t off_acc_ready(int q) { return offsetof(IpcFlags, acc_ready) + (size_t)q * 4; }
+size_t off_acc_done(int q) { return offsetof(IpcFlags, acc_done) + (size_t)q * 4; }
+#define INFCL_CU_TRY(expr)                                                                              \
+  do {                                                                                                  \
+    CUresult _r = (expr);                                                                               \
+    if (_r != CUDA_SUCCESS) return fail(INFCL_ERR_CUDA, std::string(#expr) + ": CUresult " + std::to_string((int)_r)); \
+  } while (0)
+// wait on `stream` until the local flag reaches v / write v to a flag of `region` (fenced: earlier work of the
+// stream, including copies, is visible before the flag)
+infcl_status flag_wait(cudaStream_t stream, uint8_t* region, size_t field, uint32_t v) {
+  INFCL_CU_TRY(memops().wait((CUstream)stream, reinterpret_cast<CUdeviceptr>(region + field), v,
+                             CU_STREAM_WAIT_VALUE_GEQ));
+  return INFCL_OK;
+}
+infcl_status flag_write(cudaStream_t stream, uint8_t* region, size_t field, uint32_t v) {
+  INFCL_CU_TRY(memops().write((CUstream)stream, reinterpret_cast<CUdeviceptr>(region + field), v,
+                              CU_STREAM_WRITE_VALUE_DEFAULT));
+  return INFCL_OK;
+}
+
+// send `bytes` of `src` to slot (kind, s) of rank r-1, and (NCCL) receive rank r+1's into our slot (kind, s);
+// on the comm stream
+infcl_status xsend(infcl_comm c, int kind, int s, const void* src, size_t bytes) {
   const int n = c->world, r = c->rank;
-  INFCL_NCCL_TRY(nccl().GroupStart());
-  INFCL_NCCL_TRY(nccl().Send(send, bytes, ncclUint8, prev_rank(r, n), c->comm, c->stream));
-  INFCL_NCCL_TRY(nccl().Recv(recv, bytes, ncclUint8, next_rank(r, n), c->comm, c->stream));
-  INFCL_NCCL_TRY(nccl().GroupEnd());
+  if (c->transport == INFCL_TRANSPORT_NCCL) {
+    INFCL_NCCL_TRY(nccl().GroupStart());
+    INFCL_NCCL_TRY(nccl().Send(src, bytes, ncclUint8, prev_rank(r, n), c->comm, c->stream));
+    INFCL_NCCL_TRY(nccl().Recv(c->nslot[kind][s], bytes, ncclUint8, next_rank(r, n), c->comm, c->stream));
+    INFCL_NCCL_TRY(nccl().GroupEnd());
+    INFCL_CUDA_TRY(cudaEventRecord(c->evr[kind][s], c->stream));
+    return INFCL_OK;
+  }
+  if (bytes > c->cap[kind]) return fail(INFCL_ERR_WORKSPACE, "message larger than the IPC region slot");
+  // the previous fills of rank r-1's slot (kind, s) must all have been released by r-1
+  TRY(flag_wait(c->stream, c->region, off_freed(kind, s), c->fills[kind][s]));
+  uint8_t* dst = c->peers[prev_rank(r, n)] + c->off[kind] + (size_t)s * c->cap[kind];
+  INFCL_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  ++c->fills[kind][s];
+  return flag_write(c->stream, c->peers[prev_rank(r, n)], off_ready(kind, s), c->fills[kind][s]);
+}
+// make `stream` wait until our slot (kind, s) holds the fill that pairs with our latest xsend(kind, s)
+infcl_status xwait(infcl_comm c, cudaStream_t stream, int kind, int s) {
+  if (c->transport == INFCL_TRANSPORT_NCCL) {
+    INFCL_CUDA_TRY(cudaStreamWaitEvent(stream, c->evr[kind][s], 0));
+    return INFCL_OK;
+  }
+  return flag_wait(stream, c->region, off_ready(kind, s), c->fills[kind][s]);
+}
+// our slot (kind, s) is no longer read (ordered on `stream`): rank r+1 may refill it
+infcl_status xrelease(infcl_comm c, cudaStream_t stream, int kind, int s) {
+  if (c->transport == INFCL_TRANSPORT_NCCL) return INFCL_OK;
+  ++c->rels[kind][s];
+  return flag_write(stream, c->peers[next_rank(c->rank, c->world)], off_freed(kind, s), c->rels[kind][s]);
+}
+// sum of one fp64 per rank into `acc` on every rank, in rank order (deterministic); on the comm stream
+infcl_status allreduce_acc(infcl_comm c, double* acc) {
+  if (c->transport == INFCL_TRANSPORT_NCCL) {
+    INFCL_NCCL_TRY(nccl().AllReduce(acc, acc, 1, ncclFloat64, ncclSum, c->comm, c->stream));
+    return INFCL_OK;
+  }
+  const int n = c->world, r = c->rank;
+  const uint32_t call = ++c->calls;
+  for (int q = 0; q < n; ++q) {  // deposit our partial in acc_in[r] of every rank (q == r: our own region)
+    if (q != r) TRY(flag_wait(c->stream, c->region, off_acc_done(q), call - 1));  // q summed the last call
+    INFCL_CUDA_TRY(cudaMemcpyAsync(c->peers[q] + offsetof(IpcFlags, acc_in) + r * sizeof(double), acc,
+                                   sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    if (q != r) TRY(flag_write(c->stream, c->peers[q], off_acc_ready(r), call));
+  }
+  for (int q = 0; q < n; ++q)
+    if (q != r) TRY(flag_wait(c->stream, c->region, off_acc_ready(q), call));
+  launch_sum_f64(reinterpret_cast<const double*>(c->region + offsetof(IpcFlags, acc_in)), n, acc, c->stream);
+  for (int q = 0; q < n; ++q)
+    if (q != r) TRY(flag_write(c->stream, c->peers[q], off_acc_done(r), call));
+  INFCL_CUDA_TRY(cudaGetLastError());
   return INFCL_OK;
 }
 // non-blocking check for an asynchronous NCCL failure on the ring (a peer died, a network error): reported as
@@ -424,23 +662,46 @@ extern "C" size_t infcl_workspace_bytes(int64_t b, int d, int world, infcl_dtype
   return make_layout(b, d, world, dt).total;
 }
 
-#define TRY(x)                      \
-  do {                              \
-    infcl_status _s = (x);          \
-    if (_s != INFCL_OK) return _s;  \
-  } while (0)
+extern "C" size_t infcl_comm_workspace_bytes(infcl_comm comm, int64_t b, int d, int world, infcl_dtype dt) {
+  if (b < 1 || d < 1 || world < 1 || b % world) return 0;
+  return make_layout(b, d, world, dt, !(comm && comm->transport == INFCL_TRANSPORT_IPC)).total;
+}
+
+namespace {
+// checks shared by the ring entry points; binds the NCCL transport's receive slots to this call's workspace
+infcl_status ring_setup(infcl_comm comm, const Rank& R, int rank, int world) {
+  if (!comm || comm->world != world || comm->rank != rank)
+    return fail(INFCL_ERR_CONFIG, "world > 1 needs a communicator with matching rank/world");
+  if (comm->transport == INFCL_TRANSPORT_IPC) {
+    if (!comm->connected) return fail(INFCL_ERR_CONFIG, "IPC communicator not connected (infcl_comm_ipc_connect)");
+    if ((size_t)R.L.bs * R.L.dk * 2 > comm->cap[XK_BLK])
+      return fail(INFCL_ERR_WORKSPACE, "shard larger than the IPC region was sized for (max_b, max_d)");
+    int dev = -1;
+    INFCL_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev != comm->device) return fail(INFCL_ERR_CONFIG, "current device differs from the communicator's");
+  } else {
+    for (int s = 0; s < 2; ++s) {
+      comm->nslot[XK_BLK][s] = R.ring_blk(s);
+      comm->nslot[XK_CS][s] = R.cstate(1 + s);
+      comm->nslot[XK_LSE][s] = R.ring_lse(s);
+    }
+  }
+  return INFCL_OK;
+}
+bool ring_in_ws(infcl_comm comm) { return !(comm && comm->transport == INFCL_TRANSPORT_IPC); }
+}  // namespace
+
 
 extern "C" infcl_status infcl_forward(infcl_comm comm, const void* I_local, const void* T_local, infcl_dtype dt,
                                       int64_t b, int d, float s, int rank, int world, float* row_lse, float* col_lse,
                                       float* diag, float* loss, void* ws, size_t ws_bytes, void* stream) {
-  const size_t need = infcl_workspace_bytes(b, d, world, dt);
+  const size_t need = infcl_comm_workspace_bytes(world > 1 ? comm : nullptr, b, d, world, dt);
   TRY(validate(I_local, T_local, dt, b, d, s, rank, world, ws, ws_bytes, need));
   if (!row_lse || !col_lse || !diag || !loss) return fail(INFCL_ERR_INVALID_ARG, "null output pointer");
-  if (world > 1 && (!comm || comm->world != world || comm->rank != rank))
-    return fail(INFCL_ERR_CONFIG, "world > 1 needs a communicator with matching rank/world");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Rank R;
-  TRY(prepare_rank(R, I_local, T_local, dt, b, d, s, world, ws, st));
+  TRY(prepare_rank(R, I_local, T_local, dt, b, d, s, world, ws, st, world == 1 || ring_in_ws(comm)));
+  if (world > 1) TRY(ring_setup(comm, R, rank, world));
   INFCL_CUDA_TRY(cudaMemsetAsync(R.acc(), 0, sizeof(double), st));
   TRY(fwd_begin(R, st));
   if (world == 1) {
@@ -451,33 +712,43 @@ extern "C" infcl_status infcl_forward(infcl_comm comm, const void* I_local, cons
     INFCL_CUDA_TRY(cudaGetLastError());
     return INFCL_OK;
   }
-  // ---- ring over `world` GPUs (Alg.1): T block prefetched one step ahead; column state follows compute
+  // ---- ring over `world` GPUs (Alg.1): the T block is prefetched one step ahead on the comm stream
+  // (exchange k lands in slot k&1 and is computed at step k+1, and forwarded by exchange k+1); the column
+  // state follows each step's compute (exchange k of the state lands in slot k&1; the last one is the hop home)
   const size_t blk_bytes = (size_t)R.L.bs * R.L.dk * 2, cs_bytes = (size_t)R.L.bs * sizeof(float2);
   const __nv_bfloat16* held = R.B;
   INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 0), st));
   INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 0), 0));  // inputs ready before the first send
   for (int k = 0; k < world; ++k) {
-    __nv_bfloat16* next = R.ring_blk(k & 1);
     if (k + 1 < world) {
-      TRY(ring_exchange(comm, held, next, blk_bytes));  // prefetch the block held at step k+1
+      // forwarding a received block: the comm stream itself must see it arrive (IPC: the fill is a remote
+      // write, not ordered on this stream; the step's st-side wait does not cover the comm stream)
+      if (k >= 1) TRY(xwait(comm, comm->stream, XK_BLK, (k - 1) & 1));
+      TRY(xsend(comm, XK_BLK, k & 1, held, blk_bytes));  // prefetch the block held at step k+1
       INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 2), comm->stream));
     }
     TRY(fwd_step_main(R, held, k == 0, diag, st));
-    if (k >= 1) INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 3), 0));  // held block's column state arrived
-    float2* cs = R.cstate(k & 1);
+    float2* cs = k == 0 ? R.cstate(0) : static_cast<float2*>(xslot(comm, XK_CS, (k - 1) & 1));
+    if (k >= 1) TRY(xwait(comm, st, XK_CS, (k - 1) & 1));  // held block's column state arrived
     fwd_step_cols(R, cs, st);
     INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 1), st));  // compute of step k done
     INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 1), 0));
-    TRY(ring_exchange(comm, cs, R.cstate((k + 1) & 1), cs_bytes));  // column state (last: return hop home)
-    INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 3), comm->stream));
-    if (k + 1 < world) INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 2), 0));  // next block arrived
-    held = next;
+    TRY(xsend(comm, XK_CS, k & 1, cs, cs_bytes));  // column state onward (last: return hop home)
+    if (k >= 1) TRY(xrelease(comm, comm->stream, XK_CS, (k - 1) & 1));
+    if (k + 1 < world) {
+      INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 2), 0));  // our forward of `held` is done
+      TRY(xwait(comm, st, XK_BLK, k & 1));                       // next block arrived
+    }
+    if (k >= 1) TRY(xrelease(comm, st, XK_BLK, (k - 1) & 1));   // computed (and forwarded) `held`
+    held = static_cast<const __nv_bfloat16*>(xslot(comm, XK_BLK, k & 1));
   }
-  INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 3), 0));  // own column state is home
-  fwd_finish(R, R.cstate(world & 1), row_lse, col_lse, diag, R.acc(), st);
+  TRY(xwait(comm, st, XK_CS, (world - 1) & 1));  // own column state is home
+  fwd_finish(R, static_cast<const float2*>(xslot(comm, XK_CS, (world - 1) & 1)), row_lse, col_lse, diag, R.acc(),
+             st);
+  TRY(xrelease(comm, st, XK_CS, (world - 1) & 1));
   INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 4), st));
   INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 4), 0));
-  INFCL_NCCL_TRY(nccl().AllReduce(R.acc(), R.acc(), 1, ncclFloat64, ncclSum, comm->comm, comm->stream));
+  TRY(allreduce_acc(comm, R.acc()));
   INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 7), comm->stream));
   INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 7), 0));
   launch_loss_write(R.acc(), loss, b, st);
@@ -490,14 +761,13 @@ static infcl_status backward_impl(infcl_comm comm, const void* I_local, const vo
                                   int64_t b, int d, float s, int rank, int world, const float* row_lse,
                                   const float* col_lse, const float* diag, const float* grad, float* dI, float* dT,
                                   void* ws, size_t ws_bytes, void* stream, cudaEvent_t dI_ready) {
-  const size_t need = infcl_workspace_bytes(b, d, world, dt);
+  const size_t need = infcl_comm_workspace_bytes(world > 1 ? comm : nullptr, b, d, world, dt);
   TRY(validate(I_local, T_local, dt, b, d, s, rank, world, ws, ws_bytes, need));
   if (!row_lse || !col_lse || !diag || !grad || !dI || !dT) return fail(INFCL_ERR_INVALID_ARG, "null pointer");
-  if (world > 1 && (!comm || comm->world != world || comm->rank != rank))
-    return fail(INFCL_ERR_CONFIG, "world > 1 needs a communicator with matching rank/world");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Rank R;
-  TRY(prepare_rank(R, I_local, T_local, dt, b, d, s, world, ws, st));
+  TRY(prepare_rank(R, I_local, T_local, dt, b, d, s, world, ws, st, world == 1 || ring_in_ws(comm)));
+  if (world > 1) TRY(ring_setup(comm, R, rank, world));
   TRY(bwd_begin(R, row_lse, col_lse, diag, grad, dI, st));
   const size_t blk_bytes = (size_t)R.L.bs * R.L.dk * 2, lse_bytes = (size_t)R.L.bs * sizeof(float);
   for (int pass = 0; pass < 2; ++pass) {
@@ -518,21 +788,31 @@ static infcl_status backward_impl(infcl_comm comm, const void* I_local, const vo
       INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 0), st));
       INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 0), 0));
       for (int k = 0; k < world; ++k) {
-        __nv_bfloat16* next = R.ring_blk(k & 1);
-        float* next2 = R.ring_lse(k & 1);
         if (k + 1 < world) {
-          if (k >= 1) {  // `next` was held at step k-1: its compute must be done before we overwrite it
+          if (k >= 1) {  // (NCCL) our slot k&1 was held at step k-1: its compute must be done before the receive
             INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 5 + ((k - 1) & 1)), 0));
           }
-          TRY(ring_exchange(comm, held, next, blk_bytes));
-          TRY(ring_exchange(comm, held2, next2, lse_bytes));
+          if (k >= 1) {  // forwarding received slots: the comm stream must see them arrive (see the forward)
+            TRY(xwait(comm, comm->stream, XK_BLK, (k - 1) & 1));
+            TRY(xwait(comm, comm->stream, XK_LSE, (k - 1) & 1));
+          }
+          TRY(xsend(comm, XK_BLK, k & 1, held, blk_bytes));
+          TRY(xsend(comm, XK_LSE, k & 1, held2, lse_bytes));
           INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 2), comm->stream));
         }
         TRY(bwd_step(R, rows, rows2, held, held2, k == 0, dst, ld_dst, grad, st));
         INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 5 + (k & 1)), st));
-        if (k + 1 < world) INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 2), 0));
-        held = next;
-        held2 = next2;
+        if (k + 1 < world) {
+          INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 2), 0));  // our forward of (held, held2) is done
+          TRY(xwait(comm, st, XK_BLK, k & 1));
+          TRY(xwait(comm, st, XK_LSE, k & 1));
+        }
+        if (k >= 1) {  // computed and forwarded (held, held2): rank r+1 may refill those slots
+          TRY(xrelease(comm, st, XK_BLK, (k - 1) & 1));
+          TRY(xrelease(comm, st, XK_LSE, (k - 1) & 1));
+        }
+        held = static_cast<const __nv_bfloat16*>(xslot(comm, XK_BLK, k & 1));
+        held2 = static_cast<const float*>(xslot(comm, XK_LSE, k & 1));
       }
     }
     TRY(pass_end(R, pass, out, diag, row_lse, col_lse, grad, st));

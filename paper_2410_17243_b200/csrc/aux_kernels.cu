@@ -134,6 +134,12 @@ __global__ void loss_write_kernel(const double* acc, float* loss, double inv2b) 
 
 __global__ void set_scalar_kernel(float* dst, float v) { *dst = v; }
 
+__global__ void sum_f64_kernel(const double* in, int n, double* out) {
+  double v = 0.0;
+  for (int i = 0; i < n; ++i) v += in[i];
+  *out = v;
+}
+
 __global__ void scale_log2_kernel(const float* __restrict__ x, float* __restrict__ y, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = x[i] * 1.4426950408889634f;
@@ -258,6 +264,10 @@ void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s
 }
 void launch_set_scalar(float* dst, float v, cudaStream_t s) {
   set_scalar_kernel<<<1, 1, 0, s>>>(dst, v);
+  ++launch_counter();
+}
+void launch_sum_f64(const double* in, int n, double* out, cudaStream_t s) {
+  sum_f64_kernel<<<1, 1, 0, s>>>(in, n, out);
   ++launch_counter();
 }
 void launch_scale_log2(const float* x, float* y, int n, cudaStream_t s) {

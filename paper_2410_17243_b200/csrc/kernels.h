@@ -72,6 +72,7 @@ void launch_loss_partial(const float* r, const float* c, const float* diag, int 
 void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s);
 void launch_scale_log2(const float* x, float* y, int n, cudaStream_t s);
 void launch_set_scalar(float* dst, float v, cudaStream_t s);
+void launch_sum_f64(const double* in, int n, double* out, cudaStream_t s);  // out = in[0] + ... + in[n-1], in order
 // exact diagonal gradient term; init = true writes it (accumulator initialisation), false adds it
 void launch_diag_term(float* dA, int ld_dA, const void* B, int ldB, int dtype_f32, const float* diag, const float* r,
                       const float* c, const float* grad, float coef_base, int n, int d, bool init, cudaStream_t s);

@@ -33,23 +33,49 @@ def _check_features(I: torch.Tensor, T: torch.Tensor):
     return I.contiguous(), T.contiguous()
 
 
-def workspace_bytes(b: int, d: int, world: int = 1, dtype=torch.bfloat16) -> int:
-    return int(L.lib().infcl_workspace_bytes(b, d, world, _DT[dtype]))
+def workspace_bytes(b: int, d: int, world: int = 1, dtype=torch.bfloat16, comm=None) -> int:
+    return int(L.lib().infcl_comm_workspace_bytes(comm.handle if comm is not None else None, b, d, world,
+                                                  _DT[dtype]))
 
 
-def alloc_workspace(b: int, d: int, world: int, dtype, device, copies: int = 1) -> torch.Tensor:
-    n = workspace_bytes(b, d, world, dtype) * copies
+def alloc_workspace(b: int, d: int, world: int, dtype, device, copies: int = 1, comm=None) -> torch.Tensor:
+    n = workspace_bytes(b, d, world, dtype, comm) * copies
     return torch.empty(max(n, 256), dtype=torch.uint8, device=device)
 
 
 class RingComm:
-    """NCCL ring communicator of the library, bootstrapped through torch.distributed (unique-id broadcast)."""
+    """Ring communicator of the library for this process group (include/infcl.h), bootstrapped through
+    torch.distributed.  transport="nccl": the library's own NCCL communicator (unique id broadcast);
+    transport="ipc": copy-engine writes into the neighbours' receive regions over CUDA IPC peer mappings
+    (handles all-gathered), sized for shards of up to max_b / world rows of max_d features."""
 
-    def __init__(self, group=None, device=None):
+    def __init__(self, group=None, device=None, transport: str = "nccl", max_b: int | None = None,
+                 max_d: int | None = None, dtype=torch.bfloat16):
         import torch.distributed as dist
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.transport = transport
         dev = torch.cuda.current_device() if device is None else device
+        self.handle = ctypes.c_void_p()
+        if transport == "ipc":
+            if max_b is None or max_d is None:
+                raise ValueError("RingComm(transport='ipc') needs max_b and max_d to size the receive region")
+            L.call("infcl_comm_init_ipc", ctypes.byref(self.handle), self.rank, self.world, dev, int(max_b),
+                   int(max_d), _DT[dtype])
+            buf = (ctypes.c_uint8 * 64)()
+            L.call("infcl_comm_ipc_handle", self.handle, ctypes.cast(buf, ctypes.c_void_p))
+            mine = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                mine = mine.cuda()
+            allh = [torch.zeros_like(mine) for _ in range(self.world)]
+            dist.all_gather(allh, mine, group=group)
+            raw = b"".join(bytes(h.cpu().tolist()) for h in allh)
+            hbuf = (ctypes.c_uint8 * len(raw)).from_buffer_copy(raw)
+            L.call("infcl_comm_ipc_connect", self.handle, ctypes.cast(hbuf, ctypes.c_void_p))
+            dist.barrier(group=group)  # every rank mapped every region before anyone writes into it
+            return
+        if transport != "nccl":
+            raise ValueError(f"unknown transport {transport!r}")
         uid = torch.zeros(128, dtype=torch.uint8)
         if self.rank == 0:
             buf = (ctypes.c_uint8 * 128)()
@@ -60,9 +86,12 @@ class RingComm:
         dist.broadcast(uid, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
         raw = bytes(uid.cpu().tolist())
         idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(raw)
-        self.handle = ctypes.c_void_p()
         L.call("infcl_comm_init", ctypes.byref(self.handle), self.rank, self.world, ctypes.cast(idbuf, ctypes.c_void_p),
                dev)
+
+    def region_bytes(self) -> int:
+        """Device bytes the library owns for this communicator (the IPC receive region; 0 for NCCL)."""
+        return int(L.lib().infcl_comm_ipc_region_bytes(self.handle)) if self.transport == "ipc" else 0
 
     def close(self):
         if self.handle:
@@ -86,7 +115,7 @@ def infcl_forward(I_local, T_local, b: int, logit_scale: float, rank: int = 0, w
     c = torch.empty_like(r)
     dg = torch.empty_like(r)
     loss = torch.empty((), device=dev, dtype=torch.float32)
-    ws = workspace if workspace is not None else alloc_workspace(b, d, world, I_local.dtype, dev)
+    ws = workspace if workspace is not None else alloc_workspace(b, d, world, I_local.dtype, dev, comm=comm)
     L.call("infcl_forward", comm.handle if comm is not None else None, I_local.data_ptr(), T_local.data_ptr(),
            _dtype_code(I_local), b, d, float(logit_scale), rank, world, r.data_ptr(), c.data_ptr(), dg.data_ptr(),
            loss.data_ptr(), ws.data_ptr(), ws.numel(), _stream())
@@ -102,7 +131,7 @@ def infcl_backward(I_local, T_local, b: int, logit_scale: float, row_lse, col_ls
     dI = torch.empty(bs, d, device=dev, dtype=torch.float32)
     dT = torch.empty_like(dI)
     g = grad_loss.detach().to(device=dev, dtype=torch.float32).reshape(()).contiguous()
-    ws = workspace if workspace is not None else alloc_workspace(b, d, world, I_local.dtype, dev)
+    ws = workspace if workspace is not None else alloc_workspace(b, d, world, I_local.dtype, dev, comm=comm)
     L.call("infcl_backward", comm.handle if comm is not None else None, I_local.data_ptr(), T_local.data_ptr(),
            _dtype_code(I_local), b, d, float(logit_scale), rank, world, row_lse.data_ptr(), col_lse.data_ptr(),
            diag.data_ptr(), g.data_ptr(), dI.data_ptr(), dT.data_ptr(), ws.data_ptr(), ws.numel(), _stream())
