@@ -223,7 +223,14 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        comm = K.RingComm(transport=args.transport, max_b=b, max_d=d)
+        try:
+            comm = K.RingComm(transport=args.transport, max_b=b, max_d=d)
+        except L.InfclError as e:  # e.g. no peer access between these GPUs: the NCCL transport still works
+            if args.transport != "ipc":
+                raise
+            print(f"bench: IPC ring transport unavailable ({e}); using NCCL", file=sys.stderr, flush=True)
+            args.transport = "nccl"
+            comm = K.RingComm(transport="nccl")
     bs = b // world
     s = args.scale
     dev = torch.device("cuda", local)

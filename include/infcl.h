@@ -195,6 +195,11 @@ infcl_status infcl_probe_umma(const void* A, const void* B, int M, int N, int K,
 infcl_status infcl_probe_mma_rate(int M, int N, int a_mn_major, int ncta, int iters, long long* out_cycles,
                                   void* stream);
 
+/* Copy-path probe (scripts/experiments/overlap_probe.py): device-to-device copy of `bytes` on `stream`;
+ * mode 0 = cudaMemcpyAsync, mode 1 = cudaMemcpyBatchAsync with cudaMemcpyFlagPreferOverlapWithCompute (the
+ * IPC ring transport's copy).  Returns the cudaError_t of the enqueue (0 = success). */
+int infcl_diag_copy(void* dst, const void* src, size_t bytes, int mode, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,7 @@ SIGNATURES = {
     "infcl_profile_read": (_i, [_i, ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_double)]),
     "infcl_probe_mma_rate": (_i, [_i, _i, _i, _i, _i, _p, _p]),
     "infcl_probe_umma": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _i, _p]),
+    "infcl_diag_copy": (_i, [_p, _p, _sz, _i, _p]),
 }
 
 _lib = None

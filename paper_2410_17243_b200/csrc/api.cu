@@ -143,6 +143,7 @@ struct infcl_comm_s {
   std::vector<uint8_t*> peers;  // mapped receive regions of every rank (peers[rank] = region)
   bool connected = false;
   uint32_t fills[XK_N][2] = {}, rels[XK_N][2] = {}, calls = 0;
+  unsigned wait_flags = CU_STREAM_WAIT_VALUE_GEQ;  // | CU_STREAM_WAIT_VALUE_FLUSH where the device supports it
 };
 
 namespace {
@@ -247,6 +248,10 @@ extern "C" infcl_status infcl_comm_init_ipc(infcl_comm* out, int rank, int world
     infcl_comm_destroy(c);
     return st;
   }
+  // peer (NVLink) writes that reached this device before a flag are made visible to the work after the wait
+  int can_flush = 0;
+  if (cudaDeviceGetAttribute(&can_flush, cudaDevAttrCanFlushRemoteWrites, device) == cudaSuccess && can_flush)
+    c->wait_flags |= CU_STREAM_WAIT_VALUE_FLUSH;
   *out = c;
   return INFCL_OK;
 }
@@ -578,15 +583,27 @@ size_t off_acc_done(int q) { return offsetof(IpcFlags, acc_done) + (size_t)q * 4
   } while (0)
 // wait on `stream` until the local flag reaches v / write v to a flag of `region` (fenced: earlier work of the
 // stream, including copies, is visible before the flag)
-infcl_status flag_wait(cudaStream_t stream, uint8_t* region, size_t field, uint32_t v) {
-  INFCL_CU_TRY(memops().wait((CUstream)stream, reinterpret_cast<CUdeviceptr>(region + field), v,
-                             CU_STREAM_WAIT_VALUE_GEQ));
+infcl_status flag_wait(infcl_comm c, cudaStream_t stream, size_t field, uint32_t v) {
+  INFCL_CU_TRY(memops().wait((CUstream)stream, reinterpret_cast<CUdeviceptr>(c->region + field), v, c->wait_flags));
   return INFCL_OK;
 }
 infcl_status flag_write(cudaStream_t stream, uint8_t* region, size_t field, uint32_t v) {
   INFCL_CU_TRY(memops().write((CUstream)stream, reinterpret_cast<CUdeviceptr>(region + field), v,
                               CU_STREAM_WRITE_VALUE_DEFAULT));
   return INFCL_OK;
+}
+
+// device-to-device copy on the copy engines: cudaMemcpyBatchAsync with cudaMemcpyFlagPreferOverlapWithCompute
+// (a plain cudaMemcpyAsync of device memory may run as an SM copy kernel, which cannot start while the pair
+// kernels hold every SM -- scripts/experiments/overlap_probe.py measures both)
+cudaError_t ce_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  cudaMemcpyAttributes at = {};
+  at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  void* dsts[1] = {dst};
+  void* srcs[1] = {const_cast<void*>(src)};
+  size_t sizes[1] = {bytes}, idx[1] = {0}, fail_idx = 0;
+  return cudaMemcpyBatchAsync(dsts, srcs, sizes, 1, &at, idx, 1, &fail_idx, st);
 }
 
 // send `bytes` of `src` to slot (kind, s) of rank r-1, and (NCCL) receive rank r+1's into our slot (kind, s);
@@ -603,9 +620,9 @@ infcl_status xsend(infcl_comm c, int kind, int s, const void* src, size_t bytes)
   }
   if (bytes > c->cap[kind]) return fail(INFCL_ERR_WORKSPACE, "message larger than the IPC region slot");
   // the previous fills of rank r-1's slot (kind, s) must all have been released by r-1
-  TRY(flag_wait(c->stream, c->region, off_freed(kind, s), c->fills[kind][s]));
+  TRY(flag_wait(c, c->stream, off_freed(kind, s), c->fills[kind][s]));
   uint8_t* dst = c->peers[prev_rank(r, n)] + c->off[kind] + (size_t)s * c->cap[kind];
-  INFCL_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  INFCL_CUDA_TRY(ce_copy(dst, src, bytes, c->stream));
   ++c->fills[kind][s];
   return flag_write(c->stream, c->peers[prev_rank(r, n)], off_ready(kind, s), c->fills[kind][s]);
 }
@@ -615,7 +632,7 @@ infcl_status xwait(infcl_comm c, cudaStream_t stream, int kind, int s) {
     INFCL_CUDA_TRY(cudaStreamWaitEvent(stream, c->evr[kind][s], 0));
     return INFCL_OK;
   }
-  return flag_wait(stream, c->region, off_ready(kind, s), c->fills[kind][s]);
+  return flag_wait(c, stream, off_ready(kind, s), c->fills[kind][s]);
 }
 // our slot (kind, s) is no longer read (ordered on `stream`): rank r+1 may refill it
 infcl_status xrelease(infcl_comm c, cudaStream_t stream, int kind, int s) {
@@ -632,13 +649,13 @@ infcl_status allreduce_acc(infcl_comm c, double* acc) {
   const int n = c->world, r = c->rank;
   const uint32_t call = ++c->calls;
   for (int q = 0; q < n; ++q) {  // deposit our partial in acc_in[r] of every rank (q == r: our own region)
-    if (q != r) TRY(flag_wait(c->stream, c->region, off_acc_done(q), call - 1));  // q summed the last call
-    INFCL_CUDA_TRY(cudaMemcpyAsync(c->peers[q] + offsetof(IpcFlags, acc_in) + r * sizeof(double), acc,
-                                   sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    if (q != r) TRY(flag_wait(c, c->stream, off_acc_done(q), call - 1));  // q summed the last call
+    INFCL_CUDA_TRY(ce_copy(c->peers[q] + offsetof(IpcFlags, acc_in) + r * sizeof(double), acc, sizeof(double),
+                           c->stream));
     if (q != r) TRY(flag_write(c->stream, c->peers[q], off_acc_ready(r), call));
   }
   for (int q = 0; q < n; ++q)
-    if (q != r) TRY(flag_wait(c->stream, c->region, off_acc_ready(q), call));
+    if (q != r) TRY(flag_wait(c, c->stream, off_acc_ready(q), call));
   launch_sum_f64(reinterpret_cast<const double*>(c->region + offsetof(IpcFlags, acc_in)), n, acc, c->stream);
   for (int q = 0; q < n; ++q)
     if (q != r) TRY(flag_write(c->stream, c->peers[q], off_acc_done(r), call));

@@ -71,8 +71,16 @@ class RingComm:
             dist.all_gather(allh, mine, group=group)
             raw = b"".join(bytes(h.cpu().tolist()) for h in allh)
             hbuf = (ctypes.c_uint8 * len(raw)).from_buffer_copy(raw)
-            L.call("infcl_comm_ipc_connect", self.handle, ctypes.cast(hbuf, ctypes.c_void_p))
-            dist.barrier(group=group)  # every rank mapped every region before anyone writes into it
+            st = L.lib().infcl_comm_ipc_connect(self.handle, ctypes.cast(hbuf, ctypes.c_void_p))
+            detail = L.lib().infcl_last_error().decode(errors="replace") if st else ""
+            # collective outcome (also the barrier: every rank mapped every region before anyone writes)
+            ok = torch.tensor([1 if st == 0 else 0], dtype=torch.int32)
+            if dist.get_backend(group) == "nccl":
+                ok = ok.cuda()
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            if int(ok.item()) != 1:
+                self.close()
+                raise L.InfclError(st or 4, "infcl_comm_ipc_connect", detail or "a peer rank failed to connect")
             return
         if transport != "nccl":
             raise ValueError(f"unknown transport {transport!r}")
