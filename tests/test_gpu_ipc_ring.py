@@ -80,3 +80,55 @@ def test_ipc_ring_multiprocess(tmp_path, b, d, world, dtype_name):
     dT = np.concatenate([p["dT"] for p in parts])
     for got, want in ((dI, rdI), (dT, rdT)):
         assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 2e-3
+
+
+def _worker_onehot(rank, world, port, b, d, K_, s, outdir):
+    if ROOT not in sys.path:
+        sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2410_17243_b200 import loss as K
+        from synth import make_onehot_device
+        torch.cuda.set_device(0)
+        bs = b // world
+        Id, Td = make_onehot_device(b, d, K_, "cuda")
+        Ii, Ti = Id[rank * bs:(rank + 1) * bs].contiguous(), Td[rank * bs:(rank + 1) * bs].contiguous()
+        del Id, Td
+        comm = K.RingComm(transport="ipc", max_b=b, max_d=d)
+        loss, r, c, dg = K.infcl_forward(Ii, Ti, b, s, rank, world, comm)
+        dI, dT = K.infcl_backward(Ii, Ti, b, s, r, c, dg, torch.tensor(1.0, device="cuda"), rank, world, comm)
+        torch.cuda.synchronize()
+        rows = np.array([0, 1, 127, 128, 4095, bs // 2, bs - 129, bs - 1])
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), loss=loss.item(), rmax=(r - r.mean()).abs().max().item(),
+                 r0=r[0].item(), c0=c[0].item(), cmax=(c - c.mean()).abs().max().item(), rows=rows + rank * bs,
+                 dI=dI[rows].cpu().numpy(), dT=dT[rows].cpu().numpy())
+        dist.barrier()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ipc_ring_cfg3_onehot_closed_form(tmp_path):
+    """cfg3's batch (b = 262144, d = 768) as a 2-process IPC ring on one GPU (b_s = 131072: 201-MB blocks in
+    the receive slots), checked against the one-hot closed form (oracle.onehot_closed_form; exact at any b)."""
+    b, d, K_, s, world = 262144, 768, 512, 1.0, 2
+    mp.start_processes(_worker_onehot, args=(world, _free_port(), b, d, K_, s, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    parts = [np.load(tmp_path / f"rank{q}.npz") for q in range(world)]
+    m = b // K_
+    s32 = float(np.float32(s))
+    lam = float(np.log(m * np.exp(np.float32(s)) + (b - m)))
+    p, q = np.exp(s32 - lam), np.exp(-lam)
+    for part in parts:
+        assert abs(float(part["loss"]) - (lam - s32)) <= 1e-4 * abs(lam - s32)
+        assert abs(float(part["r0"]) - lam) <= 2e-3 and abs(float(part["c0"]) - lam) <= 2e-3
+        assert float(part["rmax"]) <= 2e-3 and float(part["cmax"]) <= 2e-3
+        rows = part["rows"]
+        want = np.zeros((len(rows), d))
+        want[:, :K_] = s32 / b * m * q
+        want[np.arange(len(rows)), rows % K_] = s32 / b * (m * p - 1.0)
+        for got in (part["dI"], part["dT"]):
+            assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 2e-3
