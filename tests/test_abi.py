@@ -88,3 +88,22 @@ def test_workspace_and_e2e_scratch_sizes():
     s1 = lib.infcl_e2e_scratch_bytes(65536, 512, 0)
     # e2e scratch holds the bf16 inputs, fp32 gradients, LSE vectors and the workspace
     assert s1 >= 2 * 65536 * 512 * 2 + 2 * 65536 * 512 * 4 + w1
+
+
+def test_ipc_transport_host_checks_without_gpu():
+    """IPC ring communicator: argument checks before any device work; NULL-comm queries; the comm-aware
+    workspace equals the NCCL-layout size for a NULL comm (world 1 / NCCL)."""
+    lib = L.lib()
+    out = ctypes.c_void_p()
+    assert lib.infcl_comm_init_ipc(None, 0, 2, 0, 1024, 64, 0) == 1                   # null out
+    assert lib.infcl_comm_init_ipc(ctypes.byref(out), 0, 1, 0, 1024, 64, 0) == 3      # world < 2
+    assert lib.infcl_comm_init_ipc(ctypes.byref(out), 2, 2, 0, 1024, 64, 0) == 3      # rank out of range
+    assert lib.infcl_comm_init_ipc(ctypes.byref(out), 0, 2, 0, 1023, 64, 0) == 2      # b % world
+    assert lib.infcl_comm_init_ipc(ctypes.byref(out), 0, 2, 0, 1024, 64, 0) != 0      # no GPU here: fails loudly
+    assert not out.value
+    assert lib.infcl_comm_transport(None) == -1
+    assert lib.infcl_comm_ipc_region_bytes(None) == 0
+    assert lib.infcl_comm_ipc_handle(None, None) == 1
+    assert lib.infcl_comm_ipc_connect(None, None) == 1
+    for b, d, w in ((65536, 512, 1), (65536, 512, 8), (4096, 768, 2)):
+        assert lib.infcl_comm_workspace_bytes(None, b, d, w, 0) == lib.infcl_workspace_bytes(b, d, w, 0)
