@@ -3,8 +3,9 @@
 * cfg2 (b=65536, d=512, bf16, 1 GPU) on random paired inputs: every r_i, c_j and the loss against the exact fp64
   oracle streamed over row chunks, and 256 stratified gradient rows of dI and dT against the exact fp64 rows
   (oracle.sampled_row_grads with the oracle's own r, c).
-* cfg3 (b=262144, d=768) at n=1 and cfg4's per-rank workload (b=1048576, d=768 through the 8-rank virtual ring,
-  b_s = 131072) on structured inputs with closed forms (one-hot classes, codebook), exact at any b.
+* cfg3 (b=262144, d=768) at n=1, and cfg4's / cfg5's per-rank workloads (b = 1M / 4M, d=768, through the 8-rank
+  virtual ring: b_s = 131072 / 524288) on structured inputs with closed forms (one-hot classes, codebook), exact
+  at any b.
 """
 import numpy as np
 import pytest
@@ -55,10 +56,11 @@ def test_cfg2_full_size_random_paired():
     assert abs(a - bb) <= 1e-3 * max(abs(a), abs(bb), 1e-12)
 
 
-@pytest.mark.parametrize("b,d,world", [(262144, 768, 1), (1048576, 768, 8)])
+@pytest.mark.parametrize("b,d,world", [(262144, 768, 1), (1048576, 768, 8), (4194304, 768, 8)])
 def test_large_onehot_closed_form(b, d, world):
     """One-hot classes: r = c = log(m e^s + b - m), L = that - s, closed-form gradients (oracle.onehot_closed_form).
-    world=8 runs cfg4's exact per-rank shards (b_s = 131072) through the virtual 8-rank ring schedule."""
+    world=8 runs cfg4's / cfg5's exact per-rank shards (b_s = 131072 / 524288) through the virtual 8-rank ring
+    schedule (cfg5: the paper's 4M headline batch, ~60 GB and ~80 s on one B200)."""
     K_ = 512
     s = 1.0  # well-conditioned gradient (DESIGN.md Tolerances)
     Id, Td = make_onehot_device(b, d, K_, "cuda")
