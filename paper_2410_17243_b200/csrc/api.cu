@@ -430,21 +430,18 @@ infcl_status fwd_step_main(Rank& R, const __nv_bfloat16* held, bool own, float* 
   a.slot_ld = R.L.slot_ld;
   a.row_parts = R.rparts();
   a.diag_out = own ? diag : nullptr;
-  infcl_status s = launch_pair_forward(a, st);
-  if (s) return s;
-  launch_merge_rows(R.rparts(), R.rstate(), R.L.bs, fwd_geom(R.L.bs, R.L.bs), st);
-  return INFCL_OK;
+  return launch_pair_forward(a, st);
 }
 
-void fwd_step_cols(Rank& R, float2* held_cstate, cudaStream_t st) {
-  launch_merge_cols(R.slots(), R.L.slot_ld, held_cstate, R.L.bs, fwd_geom(R.L.bs, R.L.bs), st);
+// the step's row partials into the row state and its column slots into the held block's column state
+void fwd_step_merge(Rank& R, float2* held_cstate, cudaStream_t st) {
+  launch_merge_step(R.rparts(), R.rstate(), R.L.bs, R.slots(), R.L.slot_ld, held_cstate, R.L.bs,
+                    fwd_geom(R.L.bs, R.L.bs), st);
 }
 
 void fwd_finish(Rank& R, const float2* own_cstate, float* row_lse, float* col_lse, const float* diag, double* acc,
                 cudaStream_t st) {
-  launch_finalize_lse(R.rstate(), row_lse, nullptr, R.L.bs, st);
-  launch_finalize_lse(own_cstate, col_lse, nullptr, R.L.bs, st);
-  launch_loss_partial(row_lse, col_lse, diag, R.L.bs, acc, st);
+  launch_fwd_finish(R.rstate(), own_cstate, row_lse, col_lse, diag, R.L.bs, acc, st);
 }
 
 // ---- backward pieces
@@ -723,7 +720,7 @@ extern "C" infcl_status infcl_forward(infcl_comm comm, const void* I_local, cons
   TRY(fwd_begin(R, st));
   if (world == 1) {
     TRY(fwd_step_main(R, R.B, true, diag, st));
-    fwd_step_cols(R, R.cstate(0), st);
+    fwd_step_merge(R, R.cstate(0), st);
     fwd_finish(R, R.cstate(0), row_lse, col_lse, diag, R.acc(), st);
     launch_loss_write(R.acc(), loss, b, st);
     INFCL_CUDA_TRY(cudaGetLastError());
@@ -747,7 +744,7 @@ extern "C" infcl_status infcl_forward(infcl_comm comm, const void* I_local, cons
     TRY(fwd_step_main(R, held, k == 0, diag, st));
     float2* cs = k == 0 ? R.cstate(0) : static_cast<float2*>(xslot(comm, XK_CS, (k - 1) & 1));
     if (k >= 1) TRY(xwait(comm, st, XK_CS, (k - 1) & 1));  // held block's column state arrived
-    fwd_step_cols(R, cs, st);
+    fwd_step_merge(R, cs, st);
     INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 1), st));  // compute of step k done
     INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 1), 0));
     TRY(xsend(comm, XK_CS, k & 1, cs, cs_bytes));  // column state onward (last: return hop home)
@@ -873,7 +870,7 @@ extern "C" infcl_status infcl_forward_virtual(const void* I, const void* T, infc
   for (int k = 0; k < world; ++k) {
     for (int r = 0; r < world; ++r) {
       TRY(fwd_step_main(R[r], held[r], k == 0, diag + (size_t)r * bs, st));
-      fwd_step_cols(R[r], R[r].cstate(k & 1), st);
+      fwd_step_merge(R[r], R[r].cstate(k & 1), st);
     }
     for (int r = 0; r < world; ++r) {  // rank r receives from r+1: block and column state
       const int src = next_rank(r, world);

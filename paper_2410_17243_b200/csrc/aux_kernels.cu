@@ -40,9 +40,8 @@ __global__ void init_state_kernel(float2* st, int n) {
   if (i < n) st[i] = make_float2(-INFINITY, 0.f);
 }
 
-__global__ void merge_rows_kernel(const float2* __restrict__ parts, float2* __restrict__ state, int nrows, int n_rb,
-                                  int n_ct, int P, int rpp) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void merge_rows_body(int i, const float2* __restrict__ parts, float2* __restrict__ state,
+                                                int nrows, int n_rb, int n_ct, int P, int rpp) {
   if (i >= nrows) return;
   const int rb = i / rpp;
   const int W = n_rb / P;
@@ -59,19 +58,24 @@ __global__ void merge_rows_kernel(const float2* __restrict__ parts, float2* __re
   state[i] = acc;
 }
 
+__global__ void merge_rows_kernel(const float2* __restrict__ parts, float2* __restrict__ state, int nrows, int n_rb,
+                                  int n_ct, int P, int rpp) {
+  merge_rows_body(blockIdx.x * blockDim.x + threadIdx.x, parts, state, nrows, n_rb, n_ct, P, rpp);
+}
+
 // Column state j merges the 2P per-CTA slot partials of column j (slots of pairs whose items never touched
 // column j's tile hold stale data and are skipped).  Block = 32 columns x G slot groups: group g merges slots
 // g, g+G, ... (independent loads in flight), then the G group partials merge in a fixed order (deterministic).
 // G = 8 for wide passes (bandwidth-bound); G = 32 for the small blocks of a many-rank ring, where 8 groups left
 // the GPU under-occupied and latency-bound (23 us for 8192 columns).  With no full wave (W = 0) the forward
 // geometry has n_rb < P, so the tail bookkeeping fits 32-bit integers (64-bit kept for rectangular passes).
-template <int G>
-__global__ void __launch_bounds__(32 * G) merge_cols_kernel(const float2* __restrict__ slots, long long slot_ld,
-                                                            float2* __restrict__ state, int ncols, int n_rb,
-                                                            int n_ct, int P, int all_valid) {
-  __shared__ float2 part[G][32];
-  const int j = blockIdx.x * 32 + threadIdx.x;
-  const int g = threadIdx.y;
+template <int COLS, int G>
+__device__ __forceinline__ void merge_cols_body(int blk, const float2* __restrict__ slots, long long slot_ld,
+                                                float2* __restrict__ state, int ncols, int n_rb, int n_ct, int P,
+                                                int all_valid) {
+  __shared__ float2 part[G][COLS];
+  const int tx = threadIdx.x % COLS, g = threadIdx.x / COLS;
+  const int j = blk * COLS + tx;
   const int W = n_rb / P;
   const bool check = !(all_valid || W > 0);
   const long long T = check ? (long long)n_rb * n_ct : 0;
@@ -94,37 +98,58 @@ __global__ void __launch_bounds__(32 * G) merge_cols_kernel(const float2* __rest
       if (visited) acc = merge_ms(acc, __ldg(slots + (long long)sl * slot_ld + j));
     }
   }
-  part[g][threadIdx.x] = acc;
+  part[g][tx] = acc;
   __syncthreads();
   if (g == 0 && j < ncols) {
     float2 a = state[j];
 #pragma unroll
-    for (int k = 0; k < G; ++k) a = merge_ms(a, part[k][threadIdx.x]);
+    for (int k = 0; k < G; ++k) a = merge_ms(a, part[k][tx]);
     state[j] = a;
   }
 }
 
-__global__ void finalize_lse_kernel(const float2* __restrict__ st, float* __restrict__ lse, float* __restrict__ lse2,
-                                    int n) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const float2 s = st[i];
-  const float l2 = (s.x == -INFINITY) ? -INFINITY : s.x + log2f(s.y);
-  if (lse) lse[i] = l2 * 0.69314718055994531f;
-  if (lse2) lse2[i] = l2;
+template <int COLS, int G>
+__global__ void __launch_bounds__(256) merge_cols_kernel(const float2* __restrict__ slots, long long slot_ld,
+                                                         float2* __restrict__ state, int ncols, int n_rb, int n_ct,
+                                                         int P, int all_valid) {
+  merge_cols_body<COLS, G>(blockIdx.x, slots, slot_ld, state, ncols, n_rb, n_ct, P, all_valid);
 }
 
-__global__ void loss_partial_kernel(const float* __restrict__ r, const float* __restrict__ c,
-                                    const float* __restrict__ diag, int n, double* acc) {
+// One ring step's two merges in one launch: blocks [0, nbr) fold the step's row partials into the row state
+// (merge_rows), the rest fold the per-CTA column slots into the travelling column state (merge_cols).
+template <int COLS, int G>
+__global__ void __launch_bounds__(256) merge_step_kernel(const float2* __restrict__ parts, float2* __restrict__ rstate,
+                                                         int nrows, int rn_rb, int rn_ct, int rP, int rpp, int nbr,
+                                                         const float2* __restrict__ slots, long long slot_ld,
+                                                         float2* __restrict__ cstate, int ncols, int n_rb, int n_ct,
+                                                         int P) {
+  if ((int)blockIdx.x < nbr) {
+    merge_rows_body(blockIdx.x * 256 + threadIdx.x, parts, rstate, nrows, rn_rb, rn_ct, rP, rpp);
+  } else {
+    merge_cols_body<COLS, G>(blockIdx.x - nbr, slots, slot_ld, cstate, ncols, n_rb, n_ct, P, 0);
+  }
+}
+
+// End of the forward: r_i, c_i from the row / column states, and the rank's loss partial
+// sum_i (r_i + c_i - 2 x_ii) (fp64, block reduction + one atomic per block): finalize x2 + loss_partial fused.
+__global__ void __launch_bounds__(256) fwd_finish_kernel(const float2* __restrict__ rst, const float2* __restrict__ cst,
+                                                         float* __restrict__ r, float* __restrict__ c,
+                                                         const float* __restrict__ diag, int n, double* acc) {
   double v = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    v += (double)r[i] + (double)c[i] - 2.0 * (double)diag[i];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float2 a = rst[i], b = cst[i];
+    const float ri = (a.x == -INFINITY ? -INFINITY : a.x + log2f(a.y)) * 0.69314718055994531f;
+    const float ci = (b.x == -INFINITY ? -INFINITY : b.x + log2f(b.y)) * 0.69314718055994531f;
+    r[i] = ri;
+    c[i] = ci;
+    v += (double)ri + (double)ci - 2.0 * (double)diag[i];
+  }
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __shared__ double ws[32];
+  __shared__ double ws[8];
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
   __syncthreads();
   if (threadIdx.x < 32) {
-    v = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+    v = threadIdx.x < 8 ? ws[threadIdx.x] : 0.0;
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (threadIdx.x == 0) atomicAdd(acc, v);
   }
@@ -242,20 +267,32 @@ void launch_merge_rows(const float2* parts, float2* state, int nrows, const Pass
 }
 void launch_merge_cols(const float2* slots, long long slot_ld, float2* state, int ncols, const PassGeom& g,
                        cudaStream_t s, bool all_valid) {
+  // 32 columns x 8 slot groups for wide merges (bandwidth-bound); 8 columns x 32 groups below 32768 columns,
+  // where 8 groups left the GPU under-occupied and latency-bound (23 us for 8192 columns)
   if (ncols >= 32768)
-    merge_cols_kernel<8><<<nblk(ncols, 32), dim3(32, 8), 0, s>>>(slots, slot_ld, state, ncols, g.n_rb, g.n_ct,
-                                                                 g.npairs, all_valid ? 1 : 0);
+    merge_cols_kernel<32, 8><<<nblk(ncols, 32), 256, 0, s>>>(slots, slot_ld, state, ncols, g.n_rb, g.n_ct, g.npairs,
+                                                             all_valid ? 1 : 0);
   else
-    merge_cols_kernel<32><<<nblk(ncols, 32), dim3(32, 32), 0, s>>>(slots, slot_ld, state, ncols, g.n_rb, g.n_ct,
-                                                                   g.npairs, all_valid ? 1 : 0);
+    merge_cols_kernel<8, 32><<<nblk(ncols, 8), 256, 0, s>>>(slots, slot_ld, state, ncols, g.n_rb, g.n_ct, g.npairs,
+                                                            all_valid ? 1 : 0);
   ++launch_counter();
 }
-void launch_finalize_lse(const float2* st, float* lse, float* lse2, int n, cudaStream_t s) {
-  finalize_lse_kernel<<<nblk(n, 256), 256, 0, s>>>(st, lse, lse2, n);
+void launch_merge_step(const float2* parts, float2* rstate, int nrows, const float2* slots, long long slot_ld,
+                       float2* cstate, int ncols, const PassGeom& g, cudaStream_t s) {
+  const unsigned nbr = nblk(nrows, 256);
+  if (ncols >= 32768)
+    merge_step_kernel<32, 8><<<nbr + nblk(ncols, 32), 256, 0, s>>>(parts, rstate, nrows, g.n_rb, g.n_ct, g.npairs,
+                                                                   g.rpp, (int)nbr, slots, slot_ld, cstate, ncols,
+                                                                   g.n_rb, g.n_ct, g.npairs);
+  else
+    merge_step_kernel<8, 32><<<nbr + nblk(ncols, 8), 256, 0, s>>>(parts, rstate, nrows, g.n_rb, g.n_ct, g.npairs,
+                                                                  g.rpp, (int)nbr, slots, slot_ld, cstate, ncols,
+                                                                  g.n_rb, g.n_ct, g.npairs);
   ++launch_counter();
 }
-void launch_loss_partial(const float* r, const float* c, const float* diag, int n, double* acc, cudaStream_t s) {
-  loss_partial_kernel<<<std::min(nblk(n, 256), 296u), 256, 0, s>>>(r, c, diag, n, acc);
+void launch_fwd_finish(const float2* rstate, const float2* cstate, float* r, float* c, const float* diag, int n,
+                       double* acc, cudaStream_t s) {
+  fwd_finish_kernel<<<std::min(nblk(n, 256), 592u), 256, 0, s>>>(rstate, cstate, r, c, diag, n, acc);
   ++launch_counter();
 }
 void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s) {

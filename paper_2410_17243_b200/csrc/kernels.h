@@ -67,8 +67,13 @@ void launch_init_state(float2* st, int n, cudaStream_t s);
 void launch_merge_rows(const float2* row_parts, float2* row_state, int nrows, const PassGeom& g, cudaStream_t s);
 void launch_merge_cols(const float2* col_slots, long long slot_ld, float2* col_state, int ncols, const PassGeom& g,
                        cudaStream_t s, bool all_valid = false);
-void launch_finalize_lse(const float2* st, float* lse, float* lse2, int n, cudaStream_t s);
-void launch_loss_partial(const float* r, const float* c, const float* diag, int n, double* acc, cudaStream_t s);
+// one ring step's row merge (rows [0, nrows) of rstate) and column merge (cstate) in one launch; g = the
+// step's forward geometry (square pass: the same geometry indexes both)
+void launch_merge_step(const float2* parts, float2* rstate, int nrows, const float2* slots, long long slot_ld,
+                       float2* cstate, int ncols, const PassGeom& g, cudaStream_t s);
+// r, c from the row / column states and the rank's loss partial into acc (finalize x2 + loss partial fused)
+void launch_fwd_finish(const float2* rstate, const float2* cstate, float* r, float* c, const float* diag, int n,
+                       double* acc, cudaStream_t s);
 void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s);
 void launch_scale_log2(const float* x, float* y, int n, cudaStream_t s);
 void launch_set_scalar(float* dst, float v, cudaStream_t s);
