@@ -90,6 +90,11 @@ infcl_status infcl_comm_init_ipc(infcl_comm* out, int rank, int world, int devic
                                  infcl_dtype dt);
 infcl_status infcl_comm_ipc_handle(infcl_comm comm, void* handle64);
 infcl_status infcl_comm_ipc_connect(infcl_comm comm, const void* handles);
+/* Collective self-test of a connected IPC comm: each rank copies 256 B into rank r-1's region and bumps its
+ * counter (the ring's copy, remote-write and wait paths), then verifies the bytes it received from r+1.
+ * Returns INFCL_ERR_CUDA (instead of hanging a later call) when a peer path fails or does not complete within
+ * timeout_ms. */
+infcl_status infcl_comm_ipc_selftest(infcl_comm comm, int timeout_ms);
 size_t infcl_comm_ipc_region_bytes(infcl_comm comm);
 /* INFCL_TRANSPORT_NCCL / INFCL_TRANSPORT_IPC, or -1 for NULL */
 int infcl_comm_transport(infcl_comm comm);

@@ -39,6 +39,7 @@ SIGNATURES = {
     "infcl_comm_init_ipc": (_i, [ctypes.POINTER(_p), _i, _i, _i, _i64, _i, _i]),
     "infcl_comm_ipc_handle": (_i, [_p, _p]),
     "infcl_comm_ipc_connect": (_i, [_p, _p]),
+    "infcl_comm_ipc_selftest": (_i, [_p, _i]),
     "infcl_comm_ipc_region_bytes": (_sz, [_p]),
     "infcl_comm_transport": (_i, [_p]),
     "infcl_forward": (_i, [_p, _p, _p, _i, _i64, _i, _f, _i, _i, _p, _p, _p, _p, _p, _sz, _p]),

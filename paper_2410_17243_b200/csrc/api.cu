@@ -12,6 +12,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstddef>
 #include <cstring>
@@ -121,6 +123,8 @@ struct IpcFlags {
   uint32_t acc_ready[64];   // written by rank q after depositing its loss partial in acc_in[q]: call count
   uint32_t acc_done[64];    // written by rank q after it summed the partials of a call: call count
   double acc_in[64];        // loss partials of every rank (the IPC all-reduce)
+  uint32_t hs;              // written by rank r+1 in the connection self-test
+  uint32_t hs_data[64];     // copied by rank r+1 in the connection self-test
 };
 constexpr size_t kFlagBytes = 4096;
 static_assert(sizeof(IpcFlags) <= kFlagBytes, "flag page");
@@ -670,6 +674,44 @@ infcl_status comm_async_check(infcl_comm c) {
   return INFCL_OK;
 }
 }  // namespace
+
+// Connection self-test (collective): every rank copies 256 B into rank r-1's region with the transport's own
+// copy path, bumps r-1's handshake counter with cuStreamWriteValue32, and waits for its own counter with
+// cuStreamWaitValue32 -- the three mechanisms of the ring -- then checks the copied bytes.  A peer path that
+// fails returns an error instead of hanging a later call: the host polls for `timeout_ms` and, on timeout,
+// releases the stream's wait by writing the counter itself.
+extern "C" infcl_status infcl_comm_ipc_selftest(infcl_comm c, int timeout_ms) {
+  if (!c || c->transport != INFCL_TRANSPORT_IPC || !c->connected)
+    return fail(INFCL_ERR_INVALID_ARG, "not a connected IPC comm");
+  INFCL_CUDA_TRY(cudaSetDevice(c->device));
+  const int n = c->world, r = c->rank;
+  uint32_t pattern[64];
+  for (int i = 0; i < 64; ++i) pattern[i] = 0x9E3779B9u * (uint32_t)(r + 1) + (uint32_t)i;
+  uint8_t* src = c->region + c->off[XK_LSE];  // own scratch: slot memory is free outside calls
+  INFCL_CUDA_TRY(cudaMemcpy(src, pattern, sizeof(pattern), cudaMemcpyHostToDevice));
+  INFCL_CUDA_TRY(ce_copy(c->peers[prev_rank(r, n)] + offsetof(IpcFlags, hs_data), src, sizeof(pattern), c->stream));
+  TRY(flag_write(c->stream, c->peers[prev_rank(r, n)], offsetof(IpcFlags, hs), 1));
+  TRY(flag_wait(c, c->stream, offsetof(IpcFlags, hs), 1));
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaError_t q;
+  while ((q = cudaStreamQuery(c->stream)) == cudaErrorNotReady) {
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(timeout_ms)) {
+      const uint32_t one = 1;  // unblock our own stream, then report
+      cudaMemcpy(c->region + offsetof(IpcFlags, hs), &one, sizeof(one), cudaMemcpyHostToDevice);
+      cudaStreamSynchronize(c->stream);
+      return fail(INFCL_ERR_CUDA, "IPC self-test timed out: rank " + std::to_string(next_rank(r, n)) +
+                                      " never signalled over its peer mapping");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  if (q != cudaSuccess) return fail(INFCL_ERR_CUDA, std::string("IPC self-test: ") + cudaGetErrorString(q));
+  uint32_t got[64];
+  INFCL_CUDA_TRY(cudaMemcpy(got, c->region + offsetof(IpcFlags, hs_data), sizeof(got), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 64; ++i)
+    if (got[i] != 0x9E3779B9u * (uint32_t)(next_rank(r, n) + 1) + (uint32_t)i)
+      return fail(INFCL_ERR_CUDA, "IPC self-test: data from rank " + std::to_string(next_rank(r, n)) + " corrupted");
+  return INFCL_OK;
+}
 
 extern "C" size_t infcl_workspace_bytes(int64_t b, int d, int world, infcl_dtype dt) {
   if (b < 1 || d < 1 || world < 1 || b % world) return 0;

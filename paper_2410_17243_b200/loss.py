@@ -73,15 +73,22 @@ class RingComm:
             hbuf = (ctypes.c_uint8 * len(raw)).from_buffer_copy(raw)
             st = L.lib().infcl_comm_ipc_connect(self.handle, ctypes.cast(hbuf, ctypes.c_void_p))
             detail = L.lib().infcl_last_error().decode(errors="replace") if st else ""
-            # collective outcome (also the barrier: every rank mapped every region before anyone writes)
-            ok = torch.tensor([1 if st == 0 else 0], dtype=torch.int32)
-            if dist.get_backend(group) == "nccl":
-                ok = ok.cuda()
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
-            if int(ok.item()) != 1:
-                self.close()
-                raise L.InfclError(st or 4, "infcl_comm_ipc_connect", detail or "a peer rank failed to connect")
-            return
+
+            def agree(status):  # collective outcome (MIN over ranks); also a barrier
+                ok = torch.tensor([1 if status == 0 else 0], dtype=torch.int32)
+                if dist.get_backend(group) == "nccl":
+                    ok = ok.cuda()
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+                return int(ok.item()) == 1
+
+            # every rank mapped every region before anyone writes into one
+            if agree(st):
+                st = L.lib().infcl_comm_ipc_selftest(self.handle, 10000)  # the ring's copy/write/wait paths
+                detail = L.lib().infcl_last_error().decode(errors="replace") if st else ""
+                if agree(st):
+                    return
+            self.close()
+            raise L.InfclError(st or 4, "IPC ring setup", detail or "a peer rank failed to connect or self-test")
         if transport != "nccl":
             raise ValueError(f"unknown transport {transport!r}")
         uid = torch.zeros(128, dtype=torch.uint8)

@@ -105,5 +105,6 @@ def test_ipc_transport_host_checks_without_gpu():
     assert lib.infcl_comm_ipc_region_bytes(None) == 0
     assert lib.infcl_comm_ipc_handle(None, None) == 1
     assert lib.infcl_comm_ipc_connect(None, None) == 1
+    assert lib.infcl_comm_ipc_selftest(None, 10) == 1
     for b, d, w in ((65536, 512, 1), (65536, 512, 8), (4096, 768, 2)):
         assert lib.infcl_comm_workspace_bytes(None, b, d, w, 0) == lib.infcl_workspace_bytes(b, d, w, 0)
