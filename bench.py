@@ -308,6 +308,16 @@ def run_ours(args):
             "algorithmic_flop_per_launch": flop_per_launch, "peak_source": peak_src,
             "step_tflops_8b2d": 8.0 * b * b * d / world / (ms_step / 1e3) / 1e12}
 
+    # ring traffic per rank and step: forward n-1 blocks + n column-state hops; backward two
+    # passes of n-1 (block + LSE) hops.  Time-averaged rate = bytes / step time (a lower bound on the link rate
+    # while transferring; the exchange overlaps the kernels)
+    ring = None
+    if world > 1:
+        rb = (world - 1) * bs * d * 2 + world * bs * 8 + 2 * (world - 1) * (bs * d * 2 + bs * 4)
+        ring = {"transport": args.transport, "bytes_per_rank_per_step": rb,
+                "avg_gb_s": rb / (ms_step / 1e3) / 1e9, "link_peak_gb_s": 900.0,
+                "avg_frac_of_link": rb / (ms_step / 1e3) / 1e9 / 900.0}
+
     # end-to-end through the public API with host buffers
     e2e = run_e2e(args, K, b, d, bs, s, rank, world, comm, dev)
 
@@ -324,6 +334,8 @@ def run_ours(args):
                           "inputs": "L2-normalised N(0,1) rows, bf16 RNE, generated on device"},
                "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "peak_gb_per_gpu": peak_gb, "loss": lval,
                "gpu_launches": launches, "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cb, "e2e": e2e}
+        if ring is not None:
+            out["ring"] = ring
         print(json.dumps(out), flush=True)
     if comm is not None:
         comm.close()
