@@ -99,6 +99,13 @@ size_t infcl_comm_ipc_region_bytes(infcl_comm comm);
 /* INFCL_TRANSPORT_NCCL / INFCL_TRANSPORT_IPC, or -1 for NULL */
 int infcl_comm_transport(infcl_comm comm);
 
+/* The per-rank ring schedule (host only, no device): the op list infcl_forward (which = 0) or one
+ * infcl_backward pass (which = 1) executes at world > 1, as int32 records of 6 {code, a, b, c, tag, 0} (codes,
+ * streams and buffer references in api.cu: OP_*, RS_*, BUF_*; slot reference = 2 * kind + s).  Writes at most
+ * `cap` records to `out` (may be NULL) and returns the count, or -1 for bad arguments.  tests/test_ring_schedule.py
+ * replays it for n ranks under both transports' semantics to check it is race- and deadlock-free. */
+int infcl_ring_schedule(int world, int rank, int which, int32_t* out, int cap);
+
 /* Bytes of device workspace infcl_forward/infcl_backward need for this configuration (0 on bad args), for the
  * NCCL transport (or world == 1).  infcl_comm_workspace_bytes: the same for the transport of `comm` (the IPC
  * transport receives into its own region, so its workspace holds no ring buffers); comm may be NULL. */

@@ -50,6 +50,7 @@ SIGNATURES = {
     "infcl_e2e_scratch_bytes": (_sz, [_i64, _i, _i]),
     "infcl_loss_grad_host": (_i, [_p, _p, _i, _i64, _i, _f, _f, _p, _p, _p, _p, _sz, _p]),
     "infcl_ring_block": (_i, [_i, _i, _i]),
+    "infcl_ring_schedule": (_i, [_i, _i, _i, ctypes.POINTER(ctypes.c_int32), _i]),
     "infcl_launch_count": (ctypes.c_uint64, []),
     "infcl_reset_launch_count": (None, []),
     "infcl_profile_enable": (None, [_i]),

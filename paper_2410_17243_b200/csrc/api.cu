@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <functional>
 #include <chrono>
 #include <thread>
 #include <cmath>
@@ -293,6 +294,8 @@ extern "C" infcl_status infcl_comm_ipc_connect(infcl_comm c, const void* handles
 }
 
 extern "C" int infcl_comm_transport(infcl_comm c) { return c ? c->transport : -1; }
+
+
 extern "C" size_t infcl_comm_ipc_region_bytes(infcl_comm c) { return c ? c->region_bytes : 0; }
 
 // ------------------------------------------------------------------------------------------ workspace
@@ -675,6 +678,157 @@ infcl_status comm_async_check(infcl_comm c) {
 }
 }  // namespace
 
+namespace {
+// ---- the ring schedule as data (Alg.1 forward, Alg.3 backward passes; readings Q13-Q15).  One generator
+// emits the per-rank op list; the executor below runs it with either transport, and infcl_ring_schedule
+// exports it so tests/test_ring_schedule.py can check it on the CPU: random interleavings of n ranks' two
+// streams under both transports' semantics must never read a slot before its fill, overwrite a slot that is
+// still to be read, or deadlock.
+enum RingOp : int32_t {
+  OP_EVREC = 1,   // a = stream, b = event
+  OP_EVWAIT = 2,  // a = stream, b = event
+  OP_SEND = 3,    // on comm: a = kind, b = slot, c = source buffer, tag = block id carried
+  OP_WAITV = 4,   // a = stream, b = kind, c = slot: the slot's pairing fill has landed
+  OP_RELEASE = 5, // a = stream, b = kind, c = slot: the slot may be refilled
+  OP_COMPUTE = 6, // on st: a = block buffer, b = LSE buffer (backward) or -9, c = step k, tag = block id
+  OP_MERGE = 7,   // on st (forward): a = column-state buffer (read-modify-write), tag = its block id
+  OP_FINISH = 8,  // on st (forward): a = column-state buffer, tag = own block id
+  OP_ALLRED = 9   // the loss all-reduce (comm stream, collective)
+};
+enum RingStream : int32_t { RS_ST = 0, RS_COMM = 1 };
+// buffer references: >= 0 a receive slot 2*kind + s; BUF_OWN the pass's own travelling block (T forward /
+// dI pass, I in the dT pass), BUF_OWNL its own LSE vector, BUF_OWNCS the own initial column state
+constexpr int32_t BUF_OWN = -1, BUF_OWNL = -2, BUF_OWNCS = -3, BUF_NONE = -9;
+struct ROp {
+  int32_t code, a, b, c, tag;
+};
+inline int32_t slot_ref(int kind, int s) { return 2 * kind + s; }
+
+void fwd_ring_ops(int n, int r, std::vector<ROp>& o) {
+  o.push_back({OP_EVREC, RS_ST, 0, 0, -1});
+  o.push_back({OP_EVWAIT, RS_COMM, 0, 0, -1});  // inputs ready before the first send
+  int32_t held = BUF_OWN;
+  for (int k = 0; k < n; ++k) {
+    const int32_t blk = (r + k) % n;  // block held at step k (reading Q13)
+    if (k + 1 < n) {
+      // forwarding a received block: the comm stream itself must see it arrive (IPC: the fill is a remote
+      // write, not ordered on this stream)
+      if (k >= 1) o.push_back({OP_WAITV, RS_COMM, XK_BLK, (k - 1) & 1, -1});
+      o.push_back({OP_SEND, XK_BLK, k & 1, held, blk});  // prefetch the block held at step k+1
+      o.push_back({OP_EVREC, RS_COMM, 2, 0, -1});
+    }
+    o.push_back({OP_COMPUTE, held, BUF_NONE, k, blk});
+    const int32_t cs = k == 0 ? BUF_OWNCS : slot_ref(XK_CS, (k - 1) & 1);
+    if (k >= 1) o.push_back({OP_WAITV, RS_ST, XK_CS, (k - 1) & 1, -1});  // held block's column state arrived
+    o.push_back({OP_MERGE, cs, 0, 0, blk});
+    o.push_back({OP_EVREC, RS_ST, 1, 0, -1});  // compute of step k done
+    o.push_back({OP_EVWAIT, RS_COMM, 1, 0, -1});
+    o.push_back({OP_SEND, XK_CS, k & 1, cs, blk});  // column state onward (last: the hop home)
+    if (k >= 1) o.push_back({OP_RELEASE, RS_COMM, XK_CS, (k - 1) & 1, -1});
+    if (k + 1 < n) {
+      o.push_back({OP_EVWAIT, RS_ST, 2, 0, -1});  // our forward of `held` is done
+      o.push_back({OP_WAITV, RS_ST, XK_BLK, k & 1, -1});  // next block arrived
+    }
+    if (k >= 1) o.push_back({OP_RELEASE, RS_ST, XK_BLK, (k - 1) & 1, -1});  // computed and forwarded `held`
+    held = slot_ref(XK_BLK, k & 1);
+  }
+  o.push_back({OP_WAITV, RS_ST, XK_CS, (n - 1) & 1, -1});  // own column state is home
+  o.push_back({OP_FINISH, slot_ref(XK_CS, (n - 1) & 1), 0, 0, r});
+  o.push_back({OP_RELEASE, RS_ST, XK_CS, (n - 1) & 1, -1});
+  o.push_back({OP_EVREC, RS_ST, 4, 0, -1});
+  o.push_back({OP_EVWAIT, RS_COMM, 4, 0, -1});
+  o.push_back({OP_ALLRED, 0, 0, 0, -1});
+  o.push_back({OP_EVREC, RS_COMM, 7, 0, -1});
+  o.push_back({OP_EVWAIT, RS_ST, 7, 0, -1});
+}
+
+// one backward pass (dI pass: rows I, streamed (T, c); dT pass: rows T, streamed (I, r)); gradients never travel
+void bwd_ring_ops(int n, int r, std::vector<ROp>& o) {
+  o.push_back({OP_EVREC, RS_ST, 0, 0, -1});
+  o.push_back({OP_EVWAIT, RS_COMM, 0, 0, -1});
+  int32_t held = BUF_OWN, held2 = BUF_OWNL;
+  for (int k = 0; k < n; ++k) {
+    const int32_t blk = (r + k) % n;
+    if (k + 1 < n) {
+      if (k >= 1) {
+        // (NCCL) our slot k&1 was held at step k-1: its compute must be done before the receive
+        o.push_back({OP_EVWAIT, RS_COMM, 5 + ((k - 1) & 1), 0, -1});
+        // forwarding received slots: the comm stream must see them arrive
+        o.push_back({OP_WAITV, RS_COMM, XK_BLK, (k - 1) & 1, -1});
+        o.push_back({OP_WAITV, RS_COMM, XK_LSE, (k - 1) & 1, -1});
+      }
+      o.push_back({OP_SEND, XK_BLK, k & 1, held, blk});
+      o.push_back({OP_SEND, XK_LSE, k & 1, held2, blk});
+      o.push_back({OP_EVREC, RS_COMM, 2, 0, -1});
+    }
+    o.push_back({OP_COMPUTE, held, held2, k, blk});
+    o.push_back({OP_EVREC, RS_ST, 5 + (k & 1), 0, -1});
+    if (k + 1 < n) {
+      o.push_back({OP_EVWAIT, RS_ST, 2, 0, -1});  // our forward of (held, held2) is done
+      o.push_back({OP_WAITV, RS_ST, XK_BLK, k & 1, -1});
+      o.push_back({OP_WAITV, RS_ST, XK_LSE, k & 1, -1});
+    }
+    if (k >= 1) {  // computed and forwarded (held, held2): rank r+1 may refill those slots
+      o.push_back({OP_RELEASE, RS_ST, XK_BLK, (k - 1) & 1, -1});
+      o.push_back({OP_RELEASE, RS_ST, XK_LSE, (k - 1) & 1, -1});
+    }
+    held = slot_ref(XK_BLK, k & 1);
+    held2 = slot_ref(XK_LSE, k & 1);
+  }
+}
+
+// executor of a ring op list on `st` (compute) and comm's stream, with comm's transport
+struct RingCtx {
+  const void* own = nullptr;   // BUF_OWN
+  const void* ownl = nullptr;  // BUF_OWNL
+  float2* owncs = nullptr;     // BUF_OWNCS
+  size_t bytes[XK_N] = {};
+  std::function<infcl_status(int k, const void* blk, const void* lse)> compute;
+  std::function<void(float2* cs)> merge;
+  std::function<void(const float2* cs)> finish;
+  double* acc = nullptr;
+};
+infcl_status run_ring(infcl_comm c, const std::vector<ROp>& ops, RingCtx& x, cudaStream_t st) {
+  auto ptr = [&](int32_t ref) -> void* {
+    if (ref == BUF_OWN) return const_cast<void*>(x.own);
+    if (ref == BUF_OWNL) return const_cast<void*>(x.ownl);
+    if (ref == BUF_OWNCS) return x.owncs;
+    return ref >= 0 ? xslot(c, ref / 2, ref % 2) : nullptr;
+  };
+  auto strm = [&](int32_t id) { return id == RS_ST ? st : c->stream; };
+  for (const ROp& op : ops) {
+    switch (op.code) {
+      case OP_EVREC: INFCL_CUDA_TRY(cudaEventRecord(ev(c, op.b), strm(op.a))); break;
+      case OP_EVWAIT: INFCL_CUDA_TRY(cudaStreamWaitEvent(strm(op.a), ev(c, op.b), 0)); break;
+      case OP_SEND: TRY(xsend(c, op.a, op.b, ptr(op.c), x.bytes[op.a])); break;
+      case OP_WAITV: TRY(xwait(c, strm(op.a), op.b, op.c)); break;
+      case OP_RELEASE: TRY(xrelease(c, strm(op.a), op.b, op.c)); break;
+      case OP_COMPUTE: TRY(x.compute(op.c, ptr(op.a), op.b == BUF_NONE ? nullptr : ptr(op.b))); break;
+      case OP_MERGE: x.merge(static_cast<float2*>(ptr(op.a))); break;
+      case OP_FINISH: x.finish(static_cast<const float2*>(ptr(op.a))); break;
+      case OP_ALLRED: TRY(allreduce_acc(c, x.acc)); break;
+      default: return fail(INFCL_ERR_INVALID_ARG, "bad ring op");
+    }
+  }
+  return INFCL_OK;
+}
+
+}  // namespace
+
+// The per-rank ring schedule as int32 records of 6 (code, a, b, c, tag, 0); which = 0 forward, 1 backward pass.
+// Returns the number of records (or -1 on bad arguments; records beyond `cap` are counted, not written).
+extern "C" int infcl_ring_schedule(int world, int rank, int which, int32_t* out, int cap) {
+  if (world < 2 || world > 64 || rank < 0 || rank >= world || which < 0 || which > 1) return -1;
+  std::vector<ROp> ops;
+  if (which == 0) fwd_ring_ops(world, rank, ops);
+  else bwd_ring_ops(world, rank, ops);
+  for (int i = 0; i < (int)ops.size() && i < cap && out; ++i) {
+    const int32_t rec[6] = {ops[i].code, ops[i].a, ops[i].b, ops[i].c, ops[i].tag, 0};
+    std::memcpy(out + 6 * (size_t)i, rec, sizeof(rec));
+  }
+  return (int)ops.size();
+}
+
 // Connection self-test (collective): every rank copies 256 B into rank r-1's region with the transport's own
 // copy path, bumps r-1's handshake counter with cuStreamWriteValue32, and waits for its own counter with
 // cuStreamWaitValue32 -- the three mechanisms of the ring -- then checks the copied bytes.  A peer path that
@@ -768,45 +922,21 @@ extern "C" infcl_status infcl_forward(infcl_comm comm, const void* I_local, cons
     INFCL_CUDA_TRY(cudaGetLastError());
     return INFCL_OK;
   }
-  // ---- ring over `world` GPUs (Alg.1): the T block is prefetched one step ahead on the comm stream
-  // (exchange k lands in slot k&1 and is computed at step k+1, and forwarded by exchange k+1); the column
-  // state follows each step's compute (exchange k of the state lands in slot k&1; the last one is the hop home)
-  const size_t blk_bytes = (size_t)R.L.bs * R.L.dk * 2, cs_bytes = (size_t)R.L.bs * sizeof(float2);
-  const __nv_bfloat16* held = R.B;
-  INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 0), st));
-  INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 0), 0));  // inputs ready before the first send
-  for (int k = 0; k < world; ++k) {
-    if (k + 1 < world) {
-      // forwarding a received block: the comm stream itself must see it arrive (IPC: the fill is a remote
-      // write, not ordered on this stream; the step's st-side wait does not cover the comm stream)
-      if (k >= 1) TRY(xwait(comm, comm->stream, XK_BLK, (k - 1) & 1));
-      TRY(xsend(comm, XK_BLK, k & 1, held, blk_bytes));  // prefetch the block held at step k+1
-      INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 2), comm->stream));
-    }
-    TRY(fwd_step_main(R, held, k == 0, diag, st));
-    float2* cs = k == 0 ? R.cstate(0) : static_cast<float2*>(xslot(comm, XK_CS, (k - 1) & 1));
-    if (k >= 1) TRY(xwait(comm, st, XK_CS, (k - 1) & 1));  // held block's column state arrived
-    fwd_step_merge(R, cs, st);
-    INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 1), st));  // compute of step k done
-    INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 1), 0));
-    TRY(xsend(comm, XK_CS, k & 1, cs, cs_bytes));  // column state onward (last: return hop home)
-    if (k >= 1) TRY(xrelease(comm, comm->stream, XK_CS, (k - 1) & 1));
-    if (k + 1 < world) {
-      INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 2), 0));  // our forward of `held` is done
-      TRY(xwait(comm, st, XK_BLK, k & 1));                       // next block arrived
-    }
-    if (k >= 1) TRY(xrelease(comm, st, XK_BLK, (k - 1) & 1));   // computed (and forwarded) `held`
-    held = static_cast<const __nv_bfloat16*>(xslot(comm, XK_BLK, k & 1));
-  }
-  TRY(xwait(comm, st, XK_CS, (world - 1) & 1));  // own column state is home
-  fwd_finish(R, static_cast<const float2*>(xslot(comm, XK_CS, (world - 1) & 1)), row_lse, col_lse, diag, R.acc(),
-             st);
-  TRY(xrelease(comm, st, XK_CS, (world - 1) & 1));
-  INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 4), st));
-  INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 4), 0));
-  TRY(allreduce_acc(comm, R.acc()));
-  INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 7), comm->stream));
-  INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 7), 0));
+  // ---- ring over `world` GPUs (Alg.1): the schedule of fwd_ring_ops, executed with comm's transport
+  std::vector<ROp> ops;
+  fwd_ring_ops(world, rank, ops);
+  RingCtx x;
+  x.own = R.B;
+  x.owncs = R.cstate(0);
+  x.bytes[XK_BLK] = (size_t)R.L.bs * R.L.dk * 2;
+  x.bytes[XK_CS] = (size_t)R.L.bs * sizeof(float2);
+  x.acc = R.acc();
+  x.compute = [&](int k, const void* blk, const void*) {
+    return fwd_step_main(R, static_cast<const __nv_bfloat16*>(blk), k == 0, diag, st);
+  };
+  x.merge = [&](float2* cs) { fwd_step_merge(R, cs, st); };
+  x.finish = [&](const float2* cs) { fwd_finish(R, cs, row_lse, col_lse, diag, R.acc(), st); };
+  TRY(run_ring(comm, ops, x, st));
   launch_loss_write(R.acc(), loss, b, st);
   TRY(comm_async_check(comm));
   INFCL_CUDA_TRY(cudaGetLastError());
@@ -839,37 +969,18 @@ static infcl_status backward_impl(infcl_comm comm, const void* I_local, const vo
     if (world == 1) {
       TRY(bwd_step(R, rows, rows2, own_blk, own_cols2, true, dst, ld_dst, grad, st));
     } else {
-      const __nv_bfloat16* held = own_blk;
-      const float* held2 = own_cols2;
-      INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 0), st));
-      INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 0), 0));
-      for (int k = 0; k < world; ++k) {
-        if (k + 1 < world) {
-          if (k >= 1) {  // (NCCL) our slot k&1 was held at step k-1: its compute must be done before the receive
-            INFCL_CUDA_TRY(cudaStreamWaitEvent(comm->stream, ev(comm, 5 + ((k - 1) & 1)), 0));
-          }
-          if (k >= 1) {  // forwarding received slots: the comm stream must see them arrive (see the forward)
-            TRY(xwait(comm, comm->stream, XK_BLK, (k - 1) & 1));
-            TRY(xwait(comm, comm->stream, XK_LSE, (k - 1) & 1));
-          }
-          TRY(xsend(comm, XK_BLK, k & 1, held, blk_bytes));
-          TRY(xsend(comm, XK_LSE, k & 1, held2, lse_bytes));
-          INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 2), comm->stream));
-        }
-        TRY(bwd_step(R, rows, rows2, held, held2, k == 0, dst, ld_dst, grad, st));
-        INFCL_CUDA_TRY(cudaEventRecord(ev(comm, 5 + (k & 1)), st));
-        if (k + 1 < world) {
-          INFCL_CUDA_TRY(cudaStreamWaitEvent(st, ev(comm, 2), 0));  // our forward of (held, held2) is done
-          TRY(xwait(comm, st, XK_BLK, k & 1));
-          TRY(xwait(comm, st, XK_LSE, k & 1));
-        }
-        if (k >= 1) {  // computed and forwarded (held, held2): rank r+1 may refill those slots
-          TRY(xrelease(comm, st, XK_BLK, (k - 1) & 1));
-          TRY(xrelease(comm, st, XK_LSE, (k - 1) & 1));
-        }
-        held = static_cast<const __nv_bfloat16*>(xslot(comm, XK_BLK, k & 1));
-        held2 = static_cast<const float*>(xslot(comm, XK_LSE, k & 1));
-      }
+      std::vector<ROp> ops;
+      bwd_ring_ops(world, rank, ops);
+      RingCtx x;
+      x.own = own_blk;
+      x.ownl = own_cols2;
+      x.bytes[XK_BLK] = blk_bytes;
+      x.bytes[XK_LSE] = lse_bytes;
+      x.compute = [&](int k, const void* blk, const void* lse) {
+        return bwd_step(R, rows, rows2, static_cast<const __nv_bfloat16*>(blk), static_cast<const float*>(lse),
+                        k == 0, dst, ld_dst, grad, st);
+      };
+      TRY(run_ring(comm, ops, x, st));
     }
     TRY(pass_end(R, pass, out, diag, row_lse, col_lse, grad, st));
     if (pass == 0 && dI_ready) INFCL_CUDA_TRY(cudaEventRecord(dI_ready, st));  // dI final: callers may copy it out
