@@ -58,7 +58,8 @@ def _worker(rank, world, port, b, d, s, dtype_name, outdir):
 
 
 @pytest.mark.parametrize("b,d,world,dtype_name", [(2 * 2048, 512, 2, "bf16"), (3 * 700, 64, 3, "bf16"),
-                                                  (4 * 1500, 128, 4, "bf16"), (2 * 320, 64, 2, "fp32")])
+                                                  (4 * 1500, 128, 4, "bf16"), (2 * 320, 64, 2, "fp32"),
+                                                  (8 * 520, 64, 8, "bf16")])
 def test_ipc_ring_multiprocess(tmp_path, b, d, world, dtype_name):
     import oracle
     from synth import make_features
