@@ -6,6 +6,9 @@
 * cfg3 (b=262144, d=768) at n=1, and cfg4's / cfg5's per-rank workloads (b = 1M / 4M, d=768, through the 8-rank
   virtual ring: b_s = 131072 / 524288) on structured inputs with closed forms (one-hot classes, codebook), exact
   at any b.
+* cfg3 on random paired inputs at n = 1 and through the 8-rank virtual ring (b_s = 32768) by the sampled
+  protocol: exact r, c at 256 stratified rows / columns, loss from the GPU's r, c and the exact diagonal, and 256
+  exact gradient rows of dI and dT.
 """
 import numpy as np
 import pytest
@@ -148,3 +151,43 @@ def test_wide_forward_waves_and_tail(b, d):
     rows = rows[rows < b]
     assert rel_norm(dI.cpu().numpy()[rows], oracle.sampled_row_grads(I, T, S, ref["r"], ref["c"], rows)) <= 2e-3
     assert rel_norm(dT.cpu().numpy()[rows], oracle.sampled_row_grads(T, I, S, ref["c"], ref["r"], rows)) <= 2e-3
+
+
+@pytest.mark.parametrize("world", [1, 8])
+def test_cfg3_random_sampled_protocol(world):
+    """cfg3 (b = 262144, d = 768) on RANDOM paired inputs by the large-b protocol: exact fp64 r_i
+    for 256 stratified rows and c_j for 256 stratified columns (O(b d) each), the loss recomputed from the GPU's
+    r, c and the exact diagonal, and 256 gradient rows of dI and dT from exact P (oracle r at those rows) and the
+    GPU's c (resp. r).  world = 8 runs cfg3's n = 8 per-rank shape (b_s = 32768) through the virtual ring."""
+    b, d = 262144, 768
+    I, T = make_features(b, d, seed=4, dist="paired")
+    Id, Td = I.cuda(), T.cuda()
+    g = torch.tensor(1.0, device="cuda")
+    if world == 1:
+        loss, r, c, dg = K.infcl_forward(Id, Td, b, S)
+        dI, dT = K.infcl_backward(Id, Td, b, S, r, c, dg, g)
+    else:
+        loss, r, c, dg = K.infcl_forward_virtual(Id, Td, S, world)
+        dI, dT = K.infcl_backward_virtual(Id, Td, S, world, r, c, dg, g)
+    torch.cuda.synchronize()
+    r, c, dg = r.cpu().numpy(), c.cpu().numpy(), dg.cpu().numpy()
+    rows = stratified_rows(b, 256, seed=1)
+    cols = stratified_rows(b, 256, seed=2)
+    I64, T64 = oracle.to_f64(I), oracle.to_f64(T)
+    s32 = float(np.float32(S))
+    r_ex = oracle.tile_lse(s32 * (I64[rows] @ T64.T))
+    c_ex = oracle.tile_lse(s32 * (T64[cols] @ I64.T))
+    assert np.abs(r[rows] - r_ex).max() <= 2e-3
+    assert np.abs(c[cols] - c_ex).max() <= 2e-3
+    diag_ex = s32 * np.einsum("ij,ij->i", I64, T64)
+    assert np.abs(dg - diag_ex).max() <= 2e-3
+    L = 0.5 * (np.sum(r.astype(np.float64) - diag_ex) + np.sum(c.astype(np.float64) - diag_ex)) / b
+    assert abs(loss.item() - L) <= 1e-4 * abs(L)
+    r_rows = np.array(r, dtype=np.float64)
+    r_rows[rows] = r_ex
+    rdI = oracle.sampled_row_grads(I, T, S, r_rows, c, rows)
+    assert rel_norm(dI.cpu().numpy()[rows], rdI) <= 2e-3
+    c_rows = np.array(c, dtype=np.float64)
+    c_rows[cols] = c_ex
+    rdT = oracle.sampled_row_grads(T, I, S, c_rows, r, cols)
+    assert rel_norm(dT.cpu().numpy()[cols], rdT) <= 2e-3
