@@ -6,7 +6,8 @@
 * cfg3 (b=262144, d=768) at n=1, and cfg4's / cfg5's per-rank workloads (b = 1M / 4M, d=768, through the 8-rank
   virtual ring: b_s = 131072 / 524288) on structured inputs with closed forms (one-hot classes, codebook), exact
   at any b.
-* cfg3 on random paired inputs at n = 1 and through the 8-rank virtual ring (b_s = 32768) by the sampled
+* cfg3 on random paired inputs at n = 1 and through the 8-rank virtual ring (b_s = 32768), and cfg4 (b = 1M)
+  through the 8-rank virtual ring, by the sampled
   protocol: exact r, c at 256 stratified rows / columns, loss from the GPU's r, c and the exact diagonal, and 256
   exact gradient rows of dI and dT.
 """
@@ -153,13 +154,14 @@ def test_wide_forward_waves_and_tail(b, d):
     assert rel_norm(dT.cpu().numpy()[rows], oracle.sampled_row_grads(T, I, S, ref["c"], ref["r"], rows)) <= 2e-3
 
 
-@pytest.mark.parametrize("world", [1, 8])
-def test_cfg3_random_sampled_protocol(world):
+@pytest.mark.parametrize("b,world", [(262144, 1), (262144, 8), (1048576, 8)])
+def test_cfg3_random_sampled_protocol(b, world):
     """cfg3 (b = 262144, d = 768) on RANDOM paired inputs by the large-b protocol: exact fp64 r_i
     for 256 stratified rows and c_j for 256 stratified columns (O(b d) each), the loss recomputed from the GPU's
     r, c and the exact diagonal, and 256 gradient rows of dI and dT from exact P (oracle r at those rows) and the
-    GPU's c (resp. r).  world = 8 runs cfg3's n = 8 per-rank shape (b_s = 32768) through the virtual ring."""
-    b, d = 262144, 768
+    GPU's c (resp. r).  world = 8 runs cfg3's / cfg4's n = 8 per-rank shapes (b_s = 32768 / 131072) through the
+    virtual ring."""
+    d = 768
     I, T = make_features(b, d, seed=4, dist="paired")
     Id, Td = I.cuda(), T.cuda()
     g = torch.tensor(1.0, device="cuda")
