@@ -56,8 +56,9 @@ typedef struct infcl_comm_s* infcl_comm;
 /* Ring transports.  NCCL: grouped ncclSend/ncclRecv (the receive buffers are in the caller's workspace).
  * IPC: one-sided copy-engine writes into the peer's library-owned receive region over CUDA IPC mappings
  * (NVLink/NVSwitch peer memory across GPUs; also valid when several ranks share one GPU), synchronised by
- * stream memory operations on 32-bit fill/release counters -- the exchange uses no SM, so it overlaps the
- * persistent compute kernels that occupy every SM. */
+ * stream memory operations on 32-bit fill/release counters.  Across GPUs the peer copies run on the copy
+ * engines, so the exchange can overlap the persistent compute kernels that occupy every SM (an NCCL kernel
+ * must wait for an SM); same-device copies do not overlap them (measured). */
 typedef enum { INFCL_TRANSPORT_NCCL = 0, INFCL_TRANSPORT_IPC = 1 } infcl_transport;
 
 const char* infcl_status_string(infcl_status s);
@@ -93,7 +94,7 @@ infcl_status infcl_comm_ipc_connect(infcl_comm comm, const void* handles);
 /* Collective self-test of a connected IPC comm: each rank copies 256 B into rank r-1's region and bumps its
  * counter (the ring's copy, remote-write and wait paths), then verifies the bytes it received from r+1.
  * Returns INFCL_ERR_CUDA (instead of hanging a later call) when a peer path fails or does not complete within
- * timeout_ms. */
+ * timeout_ms.  Call once per communicator, after infcl_comm_ipc_connect on every rank. */
 infcl_status infcl_comm_ipc_selftest(infcl_comm comm, int timeout_ms);
 size_t infcl_comm_ipc_region_bytes(infcl_comm comm);
 /* INFCL_TRANSPORT_NCCL / INFCL_TRANSPORT_IPC, or -1 for NULL */
