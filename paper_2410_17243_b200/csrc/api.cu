@@ -309,7 +309,7 @@ struct Layout {
   PassGeom g{};
   long long slot_ld = 0;
   size_t off_slots, off_rparts, off_rstate, off_cstate, off_own2, off_ring_lse, off_ring_blk, off_expA, off_expB,
-      off_dscr, off_acc, total;
+      off_dscr, off_tails, off_acc, total;
 };
 
 // ring_ws: the ring's receive buffers live in the workspace (NCCL transport); the IPC transport receives
@@ -342,6 +342,9 @@ Layout make_layout(int64_t b, int d, int world, infcl_dtype dt, bool ring_ws = t
   L.off_expA = take(L.f32 ? (size_t)L.bs * L.dk * 2 : 0);
   L.off_expB = take(L.f32 ? (size_t)L.bs * L.dk * 2 : 0);
   L.off_dscr = take(L.f32 ? (size_t)L.bs * L.dk * sizeof(float) : 0);
+  // backward: per-pair partials of split tail row blocks (< 2P slots of 128 rows x dk fp32; any row range of the
+  // pass has at most P - 1 tail row blocks), combined in pair order -> deterministic gradients
+  L.off_tails = take((size_t)(2 * L.g.npairs - 1) * kRowsPerPair * L.dk * sizeof(float));
   L.off_acc = take(64);
   L.total = o;
   return L;
@@ -392,6 +395,7 @@ struct Rank {
   }
   float* dscr() const { return reinterpret_cast<float*>(ws + L.off_dscr); }
   double* acc() const { return reinterpret_cast<double*>(ws + L.off_acc); }
+  float* tails() const { return reinterpret_cast<float*>(ws + L.off_tails); }
 };
 
 infcl_status prepare_rank(Rank& R, const void* I, const void* T, infcl_dtype dt, int64_t b, int d, float s, int world,
@@ -468,6 +472,7 @@ infcl_status bwd_step(Rank& R, const __nv_bfloat16* rowsA, const float* lse_rows
   a.d_out = R.L.dk;
   a.grad = grad;
   a.coef_base = (float)((double)R.s / (2.0 * (double)R.b));
+  a.tail_scratch = R.tails();
   return launch_pair_backward(a, st);
 }
 
@@ -522,6 +527,7 @@ infcl_status bwd_dT_chunk(Rank& R, int r0, int r1, const float* diag, const floa
   a.d_out = R.L.dk;
   a.grad = grad;
   a.coef_base = (float)((double)R.s / (2.0 * (double)R.b));
+  a.tail_scratch = R.tails();
   infcl_status s = launch_pair_backward(a, st);
   if (s) return s;
   INFCL_CUDA_TRY(cudaGetLastError());

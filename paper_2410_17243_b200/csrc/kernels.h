@@ -41,6 +41,8 @@ struct PassArgs {
   int ld_dA, d_out;
   const float* grad;      // device scalar g
   float coef_base;        // s / (2 b)
+  float* tail_scratch;    // [2 npairs - 1][128][d_out] fp32: per-pair partials of split tail row blocks (workspace),
+                          // added in pair order by launch_tail_combine (deterministic); nullptr = red.add
 };
 
 struct PassGeom {
@@ -75,6 +77,9 @@ void launch_merge_step(const float2* parts, float2* rstate, int nrows, const flo
 void launch_fwd_finish(const float2* rstate, const float2* cstate, float* r, float* c, const float* diag, int n,
                        double* acc, cudaStream_t s);
 void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s);
+// dst rows of the backward's split tail row blocks += their per-pair scratch partials, in ascending pair order
+void launch_tail_combine(const float* scratch, float* dst, int ld_dst, int nrows, int d_out, const PassGeom& g,
+                         cudaStream_t s);
 void launch_scale_log2(const float* x, float* y, int n, cudaStream_t s);
 void launch_set_scalar(float* dst, float v, cudaStream_t s);
 void launch_sum_f64(const double* in, int n, double* out, cudaStream_t s);  // out = in[0] + ... + in[n-1], in order

@@ -37,6 +37,7 @@ struct KParams {
   int ld_dA, d_out;
   const float* grad;
   float coef_base;
+  float* tail_scratch;      // backward: per-pair partials of split tail row blocks (deterministic) or nullptr
   unsigned long long* dbg;  // optional per-tag wait-cycle accumulators (INFCL_DEBUG_WAITS)
   int noepi;                // diagnostic: epilogue skips its math (results invalid; INFCL_DEBUG_NOEPI)
   int notma;                // diagnostic: producer signals stages without loading (results invalid)

@@ -467,6 +467,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         daph ^= 1;
         tc_fence_after();
         const int row0 = rb * kRowsPerPair + u * 64;
+        // a tail row block split between pairs goes to this pair's scratch slot (plain stores) and is added to
+        // dA in pair order by tail_combine_kernel: every element gets its partials in a fixed order
+        const bool tail_rb = p.tail_scratch != nullptr && rb >= S.W * S.P;
+        float* tdst = tail_rb ? p.tail_scratch + (long long)(S.pair + rb - S.W * S.P) * kRowsPerPair * p.d_out +
+                                    (long long)(u * 64) * p.d_out
+                              : nullptr;
         for (int tc = 0; tc < p.NDC; ++tc) {
           const int d = tc * 256 + (int)cta * 128 + q * 32 + lane;
           for (int c = 0; c < 2; ++c) {
@@ -474,10 +480,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tmem_ld32(laddr + 128 + tc * 128 + c * 32, y);
             tmem_ld_wait();
             if (d < p.d_out) {
+              if (tail_rb) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (row0 + c * 32 + i < p.nrows)
-                  red_add_f32(p.dA + (long long)(row0 + c * 32 + i) * p.ld_dA + d, coef * y[i]);
+                for (int i = 0; i < 32; ++i) tdst[(long long)(c * 32 + i) * p.d_out + d] = coef * y[i];
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (row0 + c * 32 + i < p.nrows)
+                    red_add_f32(p.dA + (long long)(row0 + c * 32 + i) * p.ld_dA + d, coef * y[i]);
+              }
             }
           }
         }
@@ -544,6 +555,8 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.d_out = a.d_out;
   k.grad = a.grad;
   k.coef_base = a.coef_base;
+  // deterministic tail: only where the last wave splits row blocks between pairs
+  k.tail_scratch = (BWD && a.tail_scratch && g.n_rb % g.npairs != 0) ? a.tail_scratch : nullptr;
   unsigned long long* dbg_buf = debug_buffer(s);
   const bool dbg_on = dbg_buf != nullptr;
   k.dbg = dbg_buf;
@@ -577,6 +590,7 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   kern<<<dim3(2 * g.npairs), dim3(kThreads), smem, s>>>(tmA, tmB, k);
   INFCL_CUDA_TRY(cudaGetLastError());
   profile_end(BWD ? 1 : 0, e0, s);
+  if (k.tail_scratch) launch_tail_combine(k.tail_scratch, a.dA, a.ld_dA, a.nrows, a.d_out, g, s);
   if (dbg_on) debug_report(BWD ? "BWD" : "FWD", g.npairs, s);
   ++launch_counter();
   return INFCL_OK;
