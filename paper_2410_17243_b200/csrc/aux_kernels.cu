@@ -159,30 +159,36 @@ __global__ void __launch_bounds__(256) fwd_finish_kernel(const float2* __restric
 // Backward tail: the row blocks the last wave splits between CTA pairs are drained by each pair into its own
 // scratch slot (plain stores); this kernel adds the slots of each row to dst in ascending pair order, so the
 // gradients are bitwise reproducible (a red.add per pair would add them in completion order).  Slot of
-// (pair p, tail row block rb) = p + rb - W*P (as the forward's row partials); one thread per (row, 4 features).
+// (pair p, tail row block rb) = p + rb - W*P (as the forward's row partials); one block per row.
 __global__ void tail_combine_kernel(const float4* __restrict__ scratch, float* __restrict__ dst, int ld_dst,
                                     int nrows, int d_out, int n_rb, int n_ct, int P, int rpp) {
+  // one block per tail row: the row block's sharing pairs are found once (thread 0), the threads stream the row
+  __shared__ int sp[2];
   const int W = n_rb / P;
-  const int d4 = d_out >> 2;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long row = (long long)W * P * rpp + idx / d4;
-  const int k4 = (int)(idx % d4);
+  const long long row = (long long)W * P * rpp + blockIdx.x;
   if (row >= nrows) return;
   const int rb = (int)(row / rpp);
   const long long T = (long long)(n_rb - W * P) * n_ct;
-  const long long t0 = (long long)(rb - W * P) * n_ct;
-  const int p0 = tail_pair_of(t0, T, P), p1 = tail_pair_of(t0 + n_ct - 1, T, P);
-  float4* o = reinterpret_cast<float4*>(dst + row * ld_dst) + k4;
-  float4 a = *o;
-  for (int p = p0; p <= p1; ++p) {
-    if (tail_begin(T, P, p + 1) <= tail_begin(T, P, p)) continue;  // empty range: no slot written
-    const float4 v = scratch[((long long)(p + rb - W * P) * rpp + (row % rpp)) * d4 + k4];
-    a.x += v.x;
-    a.y += v.y;
-    a.z += v.z;
-    a.w += v.w;
+  if (threadIdx.x == 0) {
+    const long long t0 = (long long)(rb - W * P) * n_ct;
+    sp[0] = tail_pair_of(t0, T, P);
+    sp[1] = tail_pair_of(t0 + n_ct - 1, T, P);
   }
-  *o = a;
+  __syncthreads();
+  const int p0 = sp[0], p1 = sp[1], d4 = d_out >> 2;
+  float4* o = reinterpret_cast<float4*>(dst + row * ld_dst);
+  for (int k4 = threadIdx.x; k4 < d4; k4 += blockDim.x) {
+    float4 a = o[k4];
+    for (int p = p0; p <= p1; ++p) {
+      if (tail_begin(T, P, p + 1) <= tail_begin(T, P, p)) continue;  // empty range: no slot written
+      const float4 v = __ldg(scratch + ((long long)(p + rb - W * P) * rpp + (row % rpp)) * d4 + k4);
+      a.x += v.x;
+      a.y += v.y;
+      a.z += v.z;
+      a.w += v.w;
+    }
+    o[k4] = a;
+  }
 }
 
 __global__ void loss_write_kernel(const double* acc, float* loss, double inv2b) { *loss = (float)(*acc * inv2b); }
@@ -330,9 +336,9 @@ void launch_tail_combine(const float* scratch, float* dst, int ld_dst, int nrows
   const int W = g.n_rb / g.npairs;
   const long long rows = (long long)nrows - (long long)W * g.npairs * g.rpp;
   if (rows <= 0) return;
-  const long long n = rows * (d_out / 4);
-  tail_combine_kernel<<<nblk(n, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(scratch), dst, ld_dst, nrows,
-                                                   d_out, g.n_rb, g.n_ct, g.npairs, g.rpp);
+  const int threads = std::min(256, std::max(32, (d_out / 4 + 31) / 32 * 32));
+  tail_combine_kernel<<<(unsigned)rows, threads, 0, s>>>(reinterpret_cast<const float4*>(scratch), dst, ld_dst,
+                                                         nrows, d_out, g.n_rb, g.n_ct, g.npairs, g.rpp);
   ++launch_counter();
 }
 void launch_loss_write(const double* acc, float* loss, int64_t b, cudaStream_t s) {
