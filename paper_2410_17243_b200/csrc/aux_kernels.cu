@@ -82,8 +82,16 @@ __device__ __forceinline__ void merge_cols_body(int blk, const float2* __restric
   const long long T = check ? (long long)n_rb * n_ct : 0;
   const bool small = T * P < (1LL << 31);  // always for the square forward passes: n_ct <= n_rb < P
   float2 acc = make_float2(-INFINITY, 0.f);
-  if (j < ncols && !check) {  // every slot holds data: unconditional loads
-    for (int sl = g; sl < 2 * P; sl += G) acc = merge_ms(acc, __ldg(slots + (long long)sl * slot_ld + j));
+  if (j < ncols && !check) {  // every slot holds data: unconditional loads, four in flight per thread
+    int sl = g;
+    for (; sl + 3 * G < 2 * P; sl += 4 * G) {
+      const float2 v0 = __ldg(slots + (long long)sl * slot_ld + j);
+      const float2 v1 = __ldg(slots + (long long)(sl + G) * slot_ld + j);
+      const float2 v2 = __ldg(slots + (long long)(sl + 2 * G) * slot_ld + j);
+      const float2 v3 = __ldg(slots + (long long)(sl + 3 * G) * slot_ld + j);
+      acc = merge_ms(merge_ms(merge_ms(merge_ms(acc, v0), v1), v2), v3);  // same order as one at a time
+    }
+    for (; sl < 2 * P; sl += G) acc = merge_ms(acc, __ldg(slots + (long long)sl * slot_ld + j));
   } else if (j < ncols) {
     const int ct = j / kColsPerTile;
     for (int sl = g; sl < 2 * P; sl += G) {
