@@ -160,7 +160,6 @@ infcl_status make_comm_stream(infcl_comm c) {
     for (auto& e : row) INFCL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   return INFCL_OK;
 }
-IpcFlags* flags_of(uint8_t* region) { return reinterpret_cast<IpcFlags*>(region); }
 }  // namespace
 
 extern "C" infcl_status infcl_get_unique_id(void* id128) {
@@ -509,8 +508,7 @@ void fwd_blocks_finish(Rank& R, cudaStream_t st) {
 
 // dT pass over stationary rows [r0, r1) of T (own block of I streamed); dT holds its exact diagonal term already
 // (diag_init)
-infcl_status bwd_dT_chunk(Rank& R, int r0, int r1, const float* diag, const float* row_lse, const float* col_lse,
-                          const float* grad, float* dT, cudaStream_t st) {
+infcl_status bwd_dT_chunk(Rank& R, int r0, int r1, const float* grad, float* dT, cudaStream_t st) {
   PassArgs a{};
   a.A = R.B + (size_t)r0 * R.L.dk;
   a.B = R.A;
@@ -1260,7 +1258,7 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     for (int k = 0; k < nch; ++k) {
       const int r0 = (int)dT_cut[k], r1 = (int)dT_cut[k + 1];
       if (r1 <= r0) continue;
-      TRY(bwd_dT_chunk(R, r0, r1, dg, r, c, lg + 1, dT, st));
+      TRY(bwd_dT_chunk(R, r0, r1, lg + 1, dT, st));
       INFCL_CUDA_TRY(cudaEventRecord(evs[12 + k], st));
       INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[12 + k], 0));
       INFCL_CUDA_TRY(cudaMemcpyAsync(dT_host + (size_t)r0 * d, dT + (size_t)r0 * d, (size_t)(r1 - r0) * d * 4,
