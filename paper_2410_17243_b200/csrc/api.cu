@@ -1174,12 +1174,20 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
   // chunk boundaries (eighths of b, 128-row aligned): the forward's first I chunk is small (its copy is exposed),
   // the dT pass's last chunk is small (its copy-out is exposed)
   auto at8 = [&](int e) { return std::min<int64_t>(b, (b * e / 8 + 127) / 128 * 128); };
-  const int64_t fwd_cut[5] = {0, at8(1), at8(4), at8(6), b};
+  auto at16 = [&](int e) { return std::min<int64_t>(b, (b * e / 16 + 127) / 128 * 128); };
+  // Forward on 4 I row chunks x 2 T column pieces as their copies land.  The available work grows with the
+  // product of the arrived rows and columns, so the first pieces are small: I in sixteenths {1, 3, 6, 6} and T
+  // in {3/8, 5/8}, copied T0 I0 I1 I2 T1 I3, blocks run in readiness order (timeline model at 55-128 GB/s:
+  // the forward ends 0.13-0.54 ms earlier than with I in eighths {1, 3, 2, 2}, T in halves, T0 I0 T1 I1 I2 I3,
+  // row-major blocks -- INFCL_E2E_OLD_SCHEDULE=1, kept for A/B).
+  const bool old_sched = getenv("INFCL_E2E_OLD_SCHEDULE") != nullptr;
+  const int64_t fwd_cut[5] = {0, old_sched ? at8(1) : at16(1), old_sched ? at8(4) : at16(4),
+                              old_sched ? at8(6) : at16(10), b};
   const int64_t dT_cut[5] = {0, at8(3), at8(5), at8(7), b};
-  const int64_t thalf = ((b + 1) / 2 + 255) / 256 * 256;  // the forward also splits T in two column halves
-  auto rows_of = [&](int k, int64_t len, int64_t& r0, int64_t& r1) {
-    r0 = std::min<int64_t>(b, k * len);
-    r1 = std::min<int64_t>(b, r0 + len);
+  const int64_t tsplit = std::min<int64_t>(b, old_sched ? ((b + 1) / 2 + 255) / 256 * 256 : (b * 3 / 8 + 255) / 256 * 256);
+  auto cols_of = [&](int h, int64_t& c0, int64_t& c1) {
+    c0 = h == 0 ? 0 : tsplit;
+    c1 = h == 0 ? tsplit : b;
   };
   INFCL_CUDA_TRY(cudaEventRecord(evs[0], st));  // scratch is free once prior work on `st` is done
   INFCL_CUDA_TRY(cudaStreamWaitEvent(cin, evs[0], 0));
@@ -1195,19 +1203,17 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     TRY(copy_in(T, T_host, 0, b));
     TRY(copy_in(I, I_host, 0, b));
     INFCL_CUDA_TRY(cudaEventRecord(evs[2], cin));
-  } else {  // copy order T0, I0, T1, I1, I2, I3: the first forward block starts after 3/8 of the input bytes
-    int64_t r0, r1;
-    rows_of(0, thalf, r0, r1);
-    TRY(copy_in(T, T_host, r0, r1));
+  } else {  // copy order T0, I0, I1, I2, T1, I3 (old: T0, I0, T1, I1, I2, I3); events: T0 1, I_k 2+k, T1 7
+    int64_t c0, c1;
+    cols_of(0, c0, c1);
+    TRY(copy_in(T, T_host, c0, c1));
     INFCL_CUDA_TRY(cudaEventRecord(evs[1], cin));
     for (int k = 0; k < nch; ++k) {
-      r0 = fwd_cut[k];
-      r1 = fwd_cut[k + 1];
-      TRY(copy_in(I, I_host, r0, r1));
+      TRY(copy_in(I, I_host, fwd_cut[k], fwd_cut[k + 1]));
       INFCL_CUDA_TRY(cudaEventRecord(evs[2 + k], cin));
-      if (k == 0) {
-        rows_of(1, thalf, r0, r1);
-        TRY(copy_in(T, T_host, r0, r1));
+      if (k == (old_sched ? 0 : 2)) {
+        cols_of(1, c0, c1);
+        TRY(copy_in(T, T_host, c0, c1));
         INFCL_CUDA_TRY(cudaEventRecord(evs[7], cin));
       }
     }
@@ -1231,15 +1237,17 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     INFCL_CUDA_TRY(cudaMemsetAsync(R.acc(), 0, sizeof(double), st));
     TRY(fwd_begin(R, st));
     fwd_blocks_begin(R, st);
-    for (int k = 0; k < nch; ++k) {
+    // block order (I chunk, T piece): readiness order for the copy order above
+    static const int kNew[8][2] = {{0, 0}, {1, 0}, {2, 0}, {0, 1}, {1, 1}, {2, 1}, {3, 0}, {3, 1}};
+    static const int kOld[8][2] = {{0, 0}, {0, 1}, {1, 0}, {1, 1}, {2, 0}, {2, 1}, {3, 0}, {3, 1}};
+    for (int i = 0; i < 2 * nch; ++i) {
+      const int k = old_sched ? kOld[i][0] : kNew[i][0], h = old_sched ? kOld[i][1] : kNew[i][1];
       const int64_t r0 = fwd_cut[k], r1 = fwd_cut[k + 1];
-      INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[2 + k], 0));  // rows [r0, r1) of I
-      for (int h = 0; h < 2; ++h) {
-        int64_t c0, c1;
-        rows_of(h, thalf, c0, c1);
-        INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[h == 0 ? 1 : 7], 0));  // columns [c0, c1) of T
-        if (r1 > r0 && c1 > c0) TRY(fwd_block(R, (int)r0, (int)r1, (int)c0, (int)c1, dg, st));
-      }
+      int64_t c0, c1;
+      cols_of(h, c0, c1);
+      INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[2 + k], 0));           // rows [r0, r1) of I
+      INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[h == 0 ? 1 : 7], 0));  // columns [c0, c1) of T
+      if (r1 > r0 && c1 > c0) TRY(fwd_block(R, (int)r0, (int)r1, (int)c0, (int)c1, dg, st));
     }
     fwd_blocks_finish(R, st);
     fwd_finish(R, R.cstate(0), r, c, dg, R.acc(), st);
