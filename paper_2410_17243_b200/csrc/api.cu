@@ -1183,7 +1183,10 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
   const bool old_sched = getenv("INFCL_E2E_OLD_SCHEDULE") != nullptr;
   const int64_t fwd_cut[5] = {0, old_sched ? at8(1) : at16(1), old_sched ? at8(4) : at16(4),
                               old_sched ? at8(6) : at16(10), b};
-  const int64_t dT_cut[5] = {0, at8(3), at8(5), at8(7), b};
+  // dT pass chunks: the last one's copy-out is exposed, so it is small (sixteenths {6, 5, 4, 1}; old: eighths
+  // {3, 2, 2, 1})
+  const int64_t dT_cut[5] = {0, old_sched ? at8(3) : at16(6), old_sched ? at8(5) : at16(11),
+                             old_sched ? at8(7) : at16(15), b};
   const int64_t tsplit = std::min<int64_t>(b, old_sched ? ((b + 1) / 2 + 255) / 256 * 256 : (b * 3 / 8 + 255) / 256 * 256);
   auto cols_of = [&](int h, int64_t& c0, int64_t& c1) {
     c0 = h == 0 ? 0 : tsplit;
