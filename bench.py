@@ -3,8 +3,9 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--b B] [--d D]
 
-N=1 runs BASELINE.json configs[1] (b=65536, d=512, bf16); N>1 (torchrun, one rank per GPU, NCCL ring) runs the
-same global batch (strong scaling).  A "step" is one full pass of the hot path: infcl_forward (fused S-tile GEMM +
+N=1 runs BASELINE.json configs[1] (b=65536, d=512, bf16); N>1 (one rank per GPU; launched under torchrun, or
+spawned by this script through torch.distributed.run when WORLD_SIZE is unset) runs the same global batch as a
+ring over the N GPUs (strong scaling: the same workload at every N).  A "step" is one full pass of the hot path: infcl_forward (fused S-tile GEMM +
 row/column LSE + diagonal, Alg.1/2) and infcl_backward (recompute + dI and dT, Alg.3/4) over the whole batch.
 Rank 0 prints ONE JSON line.  `--impl reference` times the fp64 CPU oracle (the only "reference" this paper-only
 run has) on a bounded sample of the same workload.
@@ -211,8 +212,7 @@ def run_ours(args):
     if same_gpu:
         local = 0
     if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N>1 must be launched with torchrun (one rank per GPU)")
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     comm = None
     b, d, name = workload(args, world)
@@ -238,6 +238,7 @@ def run_ours(args):
     ws = K.alloc_workspace(b, d, world, torch.bfloat16, dev, comm=comm)
     g = torch.ones((), device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    region = comm.region_bytes() if comm else 0
 
     def step():
         loss, r, c, dg = K.infcl_forward(I, T, b, s, rank, world, comm, ws)
@@ -247,7 +248,16 @@ def run_ours(args):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    # peak memory of ONE call (the paper's loss memory M_loss, Eq.9): outputs of earlier steps released,
+    # the L2-flush buffer (a benchmark artefact) excluded; counts the I, T shards, the workspace, r, c, diag,
+    # dI, dT, and the library-owned IPC receive region
+    if world > 1:
+        dist.barrier()
     torch.cuda.reset_peak_memory_stats(dev)
+    out1 = step()
+    torch.cuda.synchronize()
+    peak_call = torch.cuda.max_memory_allocated(dev) - flush.numel() + region
+    del out1
     lib = L.lib()
     stream = torch.cuda.current_stream()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -271,7 +281,7 @@ def run_ours(args):
     launches = int(lib.infcl_launch_count())
     import ctypes
     prof = {}
-    for kind in (0, 1):
+    for kind in (0, 1, 2):
         n = ctypes.c_int()
         ms = ctypes.c_double()
         L.call("infcl_profile_read", kind, ctypes.byref(n), ctypes.byref(ms))
@@ -279,19 +289,25 @@ def run_ours(args):
     lib.infcl_profile_enable(0)
     fwd_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in evs) / args.steps
     bwd_ms = sum(e1.elapsed_time(e2) for _, e1, e2 in evs) / args.steps
-    ms_step = max_over_ranks(fwd_ms + bwd_ms)
+    local_step_ms = fwd_ms + bwd_ms
+    ms_step = max_over_ranks(local_step_ms)
     fwd_ms = max_over_ranks(fwd_ms)
     bwd_ms = max_over_ranks(bwd_ms)
-    # torch-allocated peak plus the one device region the library owns (the IPC transport's receive slots)
-    peak_gb = max_over_ranks((torch.cuda.max_memory_allocated(dev) + (comm.region_bytes() if comm else 0)) / 1e9)
+    peak_gb = max_over_ranks(peak_call / 1e9)
     value = b / (ms_step / 1e3)
     lval = float(loss.item())
 
-    # roofline of the dominant kernel (the backward pair kernel: 2 launches per ring step)
+    # roofline of the dominant kernel (the backward pair kernel: 2 launches per ring step).  Denominator
+    # (B200_PROFILING.md): the BURST cuBLAS peak for a kernel in a short step, the SUSTAINED (power-capped) one
+    # only once a step lasts a second or more (b >= 512K); both fractions are reported
     peaks = measured_peaks()
-    peak = peaks.get("bf16_tflops_sustained") or 1400.0
-    peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step loop)" \
-        if "bf16_tflops_sustained" in peaks else "fallback 1.4 PF sustained (B200_PROFILING.md)"
+    burst = peaks.get("bf16_tflops") or 1590.0
+    sustained = peaks.get("bf16_tflops_sustained") or 1400.0
+    src = "MEASURED_PEAKS.json" if "bf16_tflops" in peaks else "fallback (B200_PROFILING.md)"
+    long_step = ms_step >= 1000.0
+    peak = sustained if long_step else burst
+    peak_src = f"{src} {'bf16_tflops_sustained' if long_step else 'bf16_tflops (burst)'}: step of {ms_step:.1f} ms " \
+               f"{'>=' if long_step else '<'} 1 s"
     kind = 1 if prof[1][1] >= prof[0][1] else 0
     n_l, tot_ms = prof[kind]
     avg_ms = max_over_ranks(tot_ms / max(n_l, 1))
@@ -303,10 +319,16 @@ def run_ours(args):
         kname = "pair_kernel<FWD> (S GEMM + row/col LSE + diag)"
     achieved = flop_per_launch / (avg_ms / 1e3) / 1e12
     traffic = ncu_traffic().get(f"{'bwd' if kind == 1 else 'fwd'}_{b}_{d}_{world}")
+    step_tf = 8.0 * b * b * d / world / (ms_step / 1e3) / 1e12
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic, "kernel": kname, "avg_launch_ms": avg_ms, "launches": n_l,
             "algorithmic_flop_per_launch": flop_per_launch, "peak_source": peak_src,
-            "step_tflops_8b2d": 8.0 * b * b * d / world / (ms_step / 1e3) / 1e12}
+            "frac_burst": achieved / burst, "frac_sustained": achieved / sustained,
+            "step_tflops_8b2d": step_tf, "step_frac_burst": step_tf / burst}
+    # time of the step outside the two pair kernels (small merge/finish kernels, launch gaps and, at N > 1, the
+    # ring exchange not hidden behind a kernel): per rank, max over ranks
+    kern_ms = (prof[0][1] + prof[1][1]) / args.steps
+    non_kernel_ms = max_over_ranks(local_step_ms - kern_ms)
 
     # ring traffic per rank and step: forward n-1 blocks + n column-state hops; backward two
     # passes of n-1 (block + LSE) hops.  Time-averaged rate = bytes / step time (a lower bound on the link rate
@@ -314,9 +336,20 @@ def run_ours(args):
     ring = None
     if world > 1:
         rb = (world - 1) * bs * d * 2 + world * bs * 8 + 2 * (world - 1) * (bs * d * 2 + bs * 4)
+        hops, hop_ms = prof[2]
+        hop_bytes = bs * d * 2
+        per_hop = max_over_ranks(hop_ms / max(hops, 1))
         ring = {"transport": args.transport, "bytes_per_rank_per_step": rb,
                 "avg_gb_s": rb / (ms_step / 1e3) / 1e9, "link_peak_gb_s": 900.0,
-                "avg_frac_of_link": rb / (ms_step / 1e3) / 1e9 / 900.0}
+                "avg_frac_of_link": rb / (ms_step / 1e3) / 1e9 / 900.0,
+                # per-hop comm-stream events (infcl_profile_read kind 2) around each travelling-block transfer
+                "hops_per_step": hops / args.steps, "hop_bytes": hop_bytes, "hop_ms": per_hop,
+                "hop_gb_s": hop_bytes / (per_hop / 1e3) / 1e9 if per_hop > 0 else None,
+                "hop_frac_of_link": hop_bytes / (per_hop / 1e3) / 1e9 / 900.0 if per_hop > 0 else None,
+                "hop_frac_of_measured_p2p": hop_bytes / (per_hop / 1e3) / 1e9 / 770.0 if per_hop > 0 else None,
+                # exposed comm: step time outside the pair kernels at this N minus the same quantity at N = 1
+                # (measured by bench.py --gpus 1: profiles/) -- here the raw non-kernel time per step
+                "non_kernel_ms": non_kernel_ms}
 
     # end-to-end through the public API with host buffers
     e2e = run_e2e(args, K, b, d, bs, s, rank, world, comm, dev)
@@ -332,7 +365,10 @@ def run_ours(args):
                "config": {"workload": name, "b": b, "d": d, "logit_scale": s, "parallelism": f"ring{world}" + (f"-{args.transport}" if world > 1 else ""),
                           "l2": "512 MB buffer written between timed steps (outside per-step events)",
                           "inputs": "L2-normalised N(0,1) rows, bf16 RNE, generated on device"},
-               "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "peak_gb_per_gpu": peak_gb, "loss": lval,
+               "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "non_kernel_ms": non_kernel_ms, "peak_gb_per_gpu": peak_gb,
+               "peak_gb_accounting": "one call: I,T shards + workspace + r,c,diag + dI,dT (+ IPC region); "
+                                     "outputs of earlier steps released; L2-flush buffer excluded",
+               "loss": lval,
                "gpu_launches": launches, "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cb, "e2e": e2e}
         if ring is not None:
             out["ring"] = ring
@@ -404,6 +440,17 @@ def main(argv=None):
     ap.add_argument("--transport", choices=["ipc", "nccl"], default="ipc",
                     help="ring transport for N>1: copy-engine writes over CUDA IPC peer memory (default) or NCCL P2P")
     args = ap.parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this script under torch.distributed.run (rank 0 prints the JSON line)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + \
+            (sys.argv[1:] if argv is None else list(argv))
+        raise SystemExit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

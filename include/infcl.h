@@ -188,30 +188,14 @@ int infcl_ring_block(int rank, int world, int step);
 uint64_t infcl_launch_count(void);
 void infcl_reset_launch_count(void);
 
-/* Kernel timing for bench.py / diagnostics.  While enabled, every fused pair-kernel launch is bracketed by
- * CUDA events on its launch stream (kind 0 = forward pair kernel, kind 1 = backward pair kernel).
+/* Kernel and ring timing for bench.py / diagnostics.  While enabled, every fused pair-kernel launch is bracketed
+ * by CUDA events on its launch stream (kind 0 = forward pair kernel, kind 1 = backward pair kernel), and every
+ * travelling-block hop of a ring call (world > 1) by events on the communicator's stream (kind 2: the transfer
+ * as the comm stream executes it, including its wait for the receiver's slot release).
  * infcl_profile_read waits for the recorded events and returns the launch count and the summed device
  * milliseconds since the last infcl_profile_enable(1).  Single-threaded use only. */
 void infcl_profile_enable(int on);
 infcl_status infcl_profile_read(int kind, int* launches, double* total_ms);
-
-/* ---------------------------------------------------------------------------------------------------
- * Probes (hardware self-test of the UMMA building blocks; used by tests/test_gpu_probe.py):
- * D = A * B^T for one tile, A [M][K] (a_mn_major=0) or stored as [K][M] (a_mn_major=1), B [N][K] bf16;
- * ncta = 1 or 2 (CTA pair); writes the raw TMEM image out[ncta][128 lanes][ncols] (fp32).
- * ------------------------------------------------------------------------------------------------- */
-infcl_status infcl_probe_umma(const void* A, const void* B, int M, int N, int K, int a_mn_major, int ncta,
-                              float* out, int ncols, void* stream);
-
-/* MMA issue-rate probe: one CTA (pair) issues `iters` back-to-back tcgen05.mma (bf16, K=16) of shape M x N
- * from resident smem; out_cycles (device, 2 x int64) = {issue cycles, issue-to-completion cycles}. */
-infcl_status infcl_probe_mma_rate(int M, int N, int a_mn_major, int ncta, int iters, long long* out_cycles,
-                                  void* stream);
-
-/* Copy-path probe (scripts/experiments/overlap_probe.py): device-to-device copy of `bytes` on `stream`;
- * mode 0 = cudaMemcpyAsync, mode 1 = cudaMemcpyBatchAsync with cudaMemcpyFlagPreferOverlapWithCompute (the
- * IPC ring transport's copy).  Returns the cudaError_t of the enqueue (0 = success). */
-int infcl_diag_copy(void* dst, const void* src, size_t bytes, int mode, void* stream);
 
 #ifdef __cplusplus
 }

@@ -26,6 +26,7 @@ from .infonce import (  # noqa: F401
     loss_and_grads,
     loss_only,
     streamed_forward,
+    streamed_grad_scale,
     sampled_row_grads,
     ring_schedule,
     ring_forward,

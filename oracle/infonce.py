@@ -223,6 +223,28 @@ def streamed_forward(I, T, s: float, chunk: int = 1024, row_limit: int | None = 
     return out
 
 
+def streamed_grad_scale(I, T, s: float, r, c, g: float = 1.0, chunk: int = 2048) -> float:
+    """g dL/ds = sum_ij G_ij <I_i, T_j> with G as in ``backward`` (x_ij = s <I_i, T_j> is linear in s, so
+    dL/ds = sum_ij (dL/dx_ij) x_ij / s), streamed over row chunks of X without forming dI, dT:
+    one GEMM per chunk.  r, c are the LSEs (exact ones from ``streamed_forward`` for an exact result)."""
+    I = to_f64(I)
+    T = to_f64(T)
+    s32 = _scale32(s)
+    b = I.shape[0]
+    r = np.asarray(r, dtype=np.float64)
+    c = np.asarray(c, dtype=np.float64)
+    acc = []
+    for i0 in range(0, b, chunk):
+        i1 = min(b, i0 + chunk)
+        P = I[i0:i1] @ T.T
+        Xc = s32 * P
+        G = (g / (2.0 * b)) * (np.exp(Xc - r[i0:i1, None]) + np.exp(Xc - c[None, :]))
+        rows = np.arange(i0, i1)
+        G[rows - i0, rows] -= g / b
+        acc.append(float((G * P).sum()))
+    return math.fsum(acc)
+
+
 def sampled_row_grads(A, B, s: float, lse_a, lse_b, rows, g: float = 1.0) -> np.ndarray:
     """Exact fp64 gradient rows dA_i = s * sum_j G_ij B_j for a sample of rows i of the stationary side.
     G_ij = g/(2b)(e^{x_ij - lse_a_i} + e^{x_ij - lse_b_j}) - (g/b)[i==j].  With (A,B,lse_a,lse_b) =

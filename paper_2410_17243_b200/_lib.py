@@ -55,9 +55,22 @@ SIGNATURES = {
     "infcl_reset_launch_count": (None, []),
     "infcl_profile_enable": (None, [_i]),
     "infcl_profile_read": (_i, [_i, ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_double)]),
+}
+
+# libinfcl_diag.so (include/infcl_diag.h): hardware probes and microbenchmarks, never on the product path
+DIAG_PATH = os.path.join(_HERE, "libinfcl_diag.so")
+DIAG_SIGNATURES = {
+    "infcl_diag_last_error": (ctypes.c_char_p, []),
+    "infcl_probe_umma": (_i, [_p, _p, _i, _i, _i, _i, _i, _i, _p, _i, _p]),
     "infcl_probe_mma_rate": (_i, [_i, _i, _i, _i, _i, _p, _p]),
-    "infcl_probe_umma": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _i, _p]),
+    "infcl_diag_max_clusters": (_i, [_i]),
+    "infcl_diag_tma_rate": (_i, [_p, _i, _i, _i, _i, _i, _p]),
+    "infcl_diag_tma_rate2": (_i, [_p, _i, _i, _i, _i, _i, _i, _p]),
+    "infcl_diag_tma_rate3": (_i, [_p, _i, _i, _i, _i, _i, _i, _p]),
+    "infcl_diag_walk": (_i, [_i, _i, _i, _i, _p]),
+    "infcl_diag_walk2": (_i, [_i, _i, _i, _i, _i, _p]),
     "infcl_diag_copy": (_i, [_p, _p, _sz, _i, _p]),
+    "infcl_diag_reduce_rate": (_i, [_p, _i64, _i, _i, _i, _i, _p]),
 }
 
 _lib = None
@@ -83,6 +96,30 @@ def lib():
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+_diag = None
+
+
+def diag():
+    """Load libinfcl_diag.so (probes; separate from the product library)."""
+    global _diag
+    if _diag is None:
+        if not os.path.exists(DIAG_PATH):
+            raise ImportError(f"{DIAG_PATH} missing: run `python -m paper_2410_17243_b200.build`")
+        D = ctypes.CDLL(DIAG_PATH)
+        for name, (res, args) in DIAG_SIGNATURES.items():
+            fn = getattr(D, name)
+            fn.restype = res
+            fn.argtypes = args
+        _diag = D
+    return _diag
+
+
+def diag_call(name: str, *args):
+    st = getattr(diag(), name)(*args)
+    if st != 0:
+        raise InfclError(st, name, diag().infcl_diag_last_error().decode(errors="replace"))
 
 
 def check(status: int, where: str):

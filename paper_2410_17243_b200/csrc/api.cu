@@ -804,7 +804,12 @@ infcl_status run_ring(infcl_comm c, const std::vector<ROp>& ops, RingCtx& x, cud
     switch (op.code) {
       case OP_EVREC: INFCL_CUDA_TRY(cudaEventRecord(ev(c, op.b), strm(op.a))); break;
       case OP_EVWAIT: INFCL_CUDA_TRY(cudaStreamWaitEvent(strm(op.a), ev(c, op.b), 0)); break;
-      case OP_SEND: TRY(xsend(c, op.a, op.b, ptr(op.c), x.bytes[op.a])); break;
+      case OP_SEND: {  // block hops are timed on the comm stream when profiling (infcl_profile_read kind 2)
+        cudaEvent_t e0 = op.a == XK_BLK ? profile_begin(c->stream) : nullptr;
+        TRY(xsend(c, op.a, op.b, ptr(op.c), x.bytes[op.a]));
+        profile_end(2, e0, c->stream);
+        break;
+      }
       case OP_WAITV: TRY(xwait(c, strm(op.a), op.b, op.c)); break;
       case OP_RELEASE: TRY(xrelease(c, strm(op.a), op.b, op.c)); break;
       case OP_COMPUTE: TRY(x.compute(op.c, ptr(op.a), op.b == BUF_NONE ? nullptr : ptr(op.b))); break;
@@ -888,7 +893,10 @@ infcl_status ring_setup(infcl_comm comm, const Rank& R, int rank, int world) {
     return fail(INFCL_ERR_CONFIG, "world > 1 needs a communicator with matching rank/world");
   if (comm->transport == INFCL_TRANSPORT_IPC) {
     if (!comm->connected) return fail(INFCL_ERR_CONFIG, "IPC communicator not connected (infcl_comm_ipc_connect)");
-    if ((size_t)R.L.bs * R.L.dk * 2 > comm->cap[XK_BLK])
+    // every message of the schedule must fit its slot BEFORE anything is enqueued: a failing xsend part-way
+    // through would leave the fill/release counters of the ring out of step (the next call would wait forever)
+    if ((size_t)R.L.bs * R.L.dk * 2 > comm->cap[XK_BLK] || (size_t)R.L.bs * sizeof(float2) > comm->cap[XK_CS] ||
+        (size_t)R.L.bs * sizeof(float) > comm->cap[XK_LSE] || (int64_t)R.L.bs > comm->max_b / world)
       return fail(INFCL_ERR_WORKSPACE, "shard larger than the IPC region was sized for (max_b, max_d)");
     int dev = -1;
     INFCL_CUDA_TRY(cudaGetDevice(&dev));
@@ -903,6 +911,18 @@ infcl_status ring_setup(infcl_comm comm, const Rank& R, int rank, int world) {
   return INFCL_OK;
 }
 bool ring_in_ws(infcl_comm comm) { return !(comm && comm->transport == INFCL_TRANSPORT_IPC); }
+// SM carve-out of a ring call: the NCCL transport's send/recv kernels need SMs, and the persistent pair kernels
+// hold every SM (one 320-thread CTA with ~200 KB of smem per SM), so with NCCL at world > 1 the pair kernels leave
+// INFCL_NCCL_CARVEOUT_PAIRS CTA pairs (default 2 = 4 SMs) free for the exchange to run beside the ring step's
+// kernel (survey H6; the P:216-219 overlap).  The IPC transport copies on the copy engines and needs none.
+int ring_carveout(infcl_comm comm, int world) {
+  if (world <= 1 || !comm || comm->transport != INFCL_TRANSPORT_NCCL) return 0;
+  static const int k = [] {
+    const char* e = getenv("INFCL_NCCL_CARVEOUT_PAIRS");
+    return e ? std::max(0, atoi(e)) : 2;
+  }();
+  return k;
+}
 }  // namespace
 
 
@@ -913,6 +933,7 @@ extern "C" infcl_status infcl_forward(infcl_comm comm, const void* I_local, cons
   TRY(validate(I_local, T_local, dt, b, d, s, rank, world, ws, ws_bytes, need));
   if (!row_lse || !col_lse || !diag || !loss) return fail(INFCL_ERR_INVALID_ARG, "null output pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PairCarveOut carve(ring_carveout(comm, world));  // layout and launches of this call see the same pair count
   Rank R;
   TRY(prepare_rank(R, I_local, T_local, dt, b, d, s, world, ws, st, world == 1 || ring_in_ws(comm)));
   if (world > 1) TRY(ring_setup(comm, R, rank, world));
@@ -955,6 +976,7 @@ static infcl_status backward_impl(infcl_comm comm, const void* I_local, const vo
   TRY(validate(I_local, T_local, dt, b, d, s, rank, world, ws, ws_bytes, need));
   if (!row_lse || !col_lse || !diag || !grad || !dI || !dT) return fail(INFCL_ERR_INVALID_ARG, "null pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PairCarveOut carve(ring_carveout(comm, world));
   Rank R;
   TRY(prepare_rank(R, I_local, T_local, dt, b, d, s, world, ws, st, world == 1 || ring_in_ws(comm)));
   if (world > 1) TRY(ring_setup(comm, R, rank, world));
@@ -1171,23 +1193,19 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
   // computes (dI is copied out during the whole dT pass).  fp32 inputs run unchunked (their bf16 split needs
   // the whole block).
   const int nch = (dt == INFCL_BF16 && b >= 32768) ? 4 : 1;
-  // chunk boundaries (eighths of b, 128-row aligned): the forward's first I chunk is small (its copy is exposed),
-  // the dT pass's last chunk is small (its copy-out is exposed)
-  auto at8 = [&](int e) { return std::min<int64_t>(b, (b * e / 8 + 127) / 128 * 128); };
+  // chunk boundaries (sixteenths of b, 128-row aligned): the forward's first I chunk is small (its copy is
+  // exposed), the dT pass's last chunk is small (its copy-out is exposed).  tests/test_gpu_large.py samples the
+  // rows on both sides of every boundary (same formulas).
   auto at16 = [&](int e) { return std::min<int64_t>(b, (b * e / 16 + 127) / 128 * 128); };
   // Forward on 4 I row chunks x 2 T column pieces as their copies land.  The available work grows with the
   // product of the arrived rows and columns, so the first pieces are small: I in sixteenths {1, 3, 6, 6} and T
   // in {3/8, 5/8}, copied T0 I0 I1 I2 T1 I3, blocks run in readiness order (timeline model at 55-128 GB/s:
   // the forward ends 0.13-0.54 ms earlier than with I in eighths {1, 3, 2, 2}, T in halves, T0 I0 T1 I1 I2 I3,
-  // row-major blocks -- INFCL_E2E_OLD_SCHEDULE=1, kept for A/B).
-  const bool old_sched = getenv("INFCL_E2E_OLD_SCHEDULE") != nullptr;
-  const int64_t fwd_cut[5] = {0, old_sched ? at8(1) : at16(1), old_sched ? at8(4) : at16(4),
-                              old_sched ? at8(6) : at16(10), b};
-  // dT pass chunks: the last one's copy-out is exposed, so it is small (sixteenths {6, 5, 4, 1}; old: eighths
-  // {3, 2, 2, 1})
-  const int64_t dT_cut[5] = {0, old_sched ? at8(3) : at16(6), old_sched ? at8(5) : at16(11),
-                             old_sched ? at8(7) : at16(15), b};
-  const int64_t tsplit = std::min<int64_t>(b, old_sched ? ((b + 1) / 2 + 255) / 256 * 256 : (b * 3 / 8 + 255) / 256 * 256);
+  // row-major blocks; measured -0.7 %).
+  const int64_t fwd_cut[5] = {0, at16(1), at16(4), at16(10), b};
+  // dT pass chunks: the last one's copy-out is exposed, so it is small (sixteenths {6, 5, 4, 1})
+  const int64_t dT_cut[5] = {0, at16(6), at16(11), at16(15), b};
+  const int64_t tsplit = std::min<int64_t>(b, (b * 3 / 8 + 255) / 256 * 256);
   auto cols_of = [&](int h, int64_t& c0, int64_t& c1) {
     c0 = h == 0 ? 0 : tsplit;
     c1 = h == 0 ? tsplit : b;
@@ -1206,7 +1224,7 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     TRY(copy_in(T, T_host, 0, b));
     TRY(copy_in(I, I_host, 0, b));
     INFCL_CUDA_TRY(cudaEventRecord(evs[2], cin));
-  } else {  // copy order T0, I0, I1, I2, T1, I3 (old: T0, I0, T1, I1, I2, I3); events: T0 1, I_k 2+k, T1 7
+  } else {  // copy order T0, I0, I1, I2, T1, I3; events: T0 1, I_k 2+k, T1 7
     int64_t c0, c1;
     cols_of(0, c0, c1);
     TRY(copy_in(T, T_host, c0, c1));
@@ -1214,7 +1232,7 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     for (int k = 0; k < nch; ++k) {
       TRY(copy_in(I, I_host, fwd_cut[k], fwd_cut[k + 1]));
       INFCL_CUDA_TRY(cudaEventRecord(evs[2 + k], cin));
-      if (k == (old_sched ? 0 : 2)) {
+      if (k == 2) {
         cols_of(1, c0, c1);
         TRY(copy_in(T, T_host, c0, c1));
         INFCL_CUDA_TRY(cudaEventRecord(evs[7], cin));
@@ -1241,10 +1259,9 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     TRY(fwd_begin(R, st));
     fwd_blocks_begin(R, st);
     // block order (I chunk, T piece): readiness order for the copy order above
-    static const int kNew[8][2] = {{0, 0}, {1, 0}, {2, 0}, {0, 1}, {1, 1}, {2, 1}, {3, 0}, {3, 1}};
-    static const int kOld[8][2] = {{0, 0}, {0, 1}, {1, 0}, {1, 1}, {2, 0}, {2, 1}, {3, 0}, {3, 1}};
+    static const int kOrder[8][2] = {{0, 0}, {1, 0}, {2, 0}, {0, 1}, {1, 1}, {2, 1}, {3, 0}, {3, 1}};
     for (int i = 0; i < 2 * nch; ++i) {
-      const int k = old_sched ? kOld[i][0] : kNew[i][0], h = old_sched ? kOld[i][1] : kNew[i][1];
+      const int k = kOrder[i][0], h = kOrder[i][1];
       const int64_t r0 = fwd_cut[k], r1 = fwd_cut[k + 1];
       int64_t c0, c1;
       cols_of(h, c0, c1);

@@ -3,15 +3,16 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-#include "host_utils.h"
-#include "ptx.cuh"
+#include "../host_utils.h"
+#include "../../../include/infcl_diag.h"
+#include "../ptx.cuh"
 
 namespace infcl {
 
 template <int NCTA>
 __global__ void __launch_bounds__(128, 1)
     probe_umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                      int N, int K, int a_mn, float* out, int ncols) {
+                      int N, int K, int a_mn, int fmt, float* out, int ncols) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int Mc = M / NCTA, Nc = N / NCTA, KB = K / 64;
@@ -55,7 +56,8 @@ __global__ void __launch_bounds__(128, 1)
   if (cta == 0 && threadIdx.x == 32) {
     mbar_wait(&bar_full, 0);
     tc_fence_after();
-    const uint32_t idesc = idesc_bf16(M, N, a_mn, 0);
+    // fmt bit 0 / bit 1: A / B holds fp16 (format 0 in the instruction descriptor) instead of bf16 (format 1)
+    const uint32_t idesc = idesc_bf16(M, N, a_mn, 0) & ~((fmt & 1) ? (7u << 7) : 0u) & ~((fmt & 2) ? (7u << 10) : 0u);
     for (int k = 0; k < K / 16; ++k) {
       uint64_t ad = a_mn ? smem_desc_sw128(smem_u32(sA + (k / 4) * (Mc / 64) * 8192 + (k % 4) * 2048), 8192, 1024)
                          : smem_desc_sw128(smem_u32(sA + (k / 4) * Mc * 128 + (k % 4) * 32), 16, 1024);
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(128, 1)
 using namespace infcl;
 
 extern "C" infcl_status infcl_probe_umma(const void* A, const void* B, int M, int N, int K, int a_mn_major, int ncta,
-                                         float* out, int ncols, void* stream) {
+                                         int fmt, float* out, int ncols, void* stream) {
   if (!A || !B || !out) return fail(INFCL_ERR_INVALID_ARG, "null pointer");
   if (ncta != 1 && ncta != 2) return fail(INFCL_ERR_INVALID_ARG, "ncta must be 1 or 2");
   if (K % 64 || K > 256 || M % (64 * ncta) || N % (16 * ncta) || ncols % 32 || ncols > 512)
@@ -110,10 +112,10 @@ extern "C" infcl_status infcl_probe_umma(const void* A, const void* B, int M, in
   cfg.numAttrs = 1;
   if (ncta == 1) {
     INFCL_CUDA_TRY(cudaFuncSetAttribute(probe_umma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    INFCL_CUDA_TRY(cudaLaunchKernelEx(&cfg, probe_umma_kernel<1>, ta, tb, M, N, K, a_mn_major, out, ncols));
+    INFCL_CUDA_TRY(cudaLaunchKernelEx(&cfg, probe_umma_kernel<1>, ta, tb, M, N, K, a_mn_major, fmt, out, ncols));
   } else {
     INFCL_CUDA_TRY(cudaFuncSetAttribute(probe_umma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    INFCL_CUDA_TRY(cudaLaunchKernelEx(&cfg, probe_umma_kernel<2>, ta, tb, M, N, K, a_mn_major, out, ncols));
+    INFCL_CUDA_TRY(cudaLaunchKernelEx(&cfg, probe_umma_kernel<2>, ta, tb, M, N, K, a_mn_major, fmt, out, ncols));
   }
   return INFCL_OK;
 }
@@ -726,3 +728,75 @@ extern "C" int infcl_diag_copy(void* dst, const void* src, size_t bytes, int mod
   size_t sizes[1] = {bytes}, idx[1] = {0}, fail_idx = 0;
   return (int)cudaMemcpyBatchAsync(dsts, srcs, sizes, 1, &at, idx, 1, &fail_idx, st);
 }
+
+// ------------------------------------------------------------------ L2 reduction throughput (single-pass feasibility)
+// The single-pass backward of Alg.4 would flush a per-tile fp32 dT partial (256 columns x d) into a
+// global dT that all CTA pairs of a column-synchronous wave share.  This probe measures how fast 148 SMs can
+// reduce fp32 data into global memory.  Each CTA holds `chunk_bytes` of fp32 ones in smem and adds them `iters`
+// times into `dst` (dst_floats floats, the "column tile" window):
+//   mode 0: cp.reduce.async.bulk .add.f32 (one thread, 16-KB bulk ops), every CTA at the same window offset
+//           (worst-case address contention: all pairs reduce the same tile at once);
+//   mode 1: the same, CTA b at offset (it + b) * chunk (same window, staggered);
+//   mode 2: the same, disjoint windows per CTA (dst_floats must hold nblocks windows of chunk_bytes);
+//   mode 3: red.global.add.v4.f32 from every thread (staggered like mode 1).
+// Bytes reduced = nblocks * iters * chunk_bytes; the caller times the launch.
+namespace infcl {
+__global__ void __launch_bounds__(256, 1) probe_reduce_kernel(float* dst, long long dst_floats, int chunk_bytes,
+                                                              int iters, int mode) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* src = reinterpret_cast<float*>(smem_raw);
+  const int nf = chunk_bytes / 4;
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) src[i] = 1.0f;
+  fence_proxy_async_smem();
+  __syncthreads();
+  const long long win = mode == 2 ? dst_floats / gridDim.x : dst_floats;
+  float* base = mode == 2 ? dst + (long long)blockIdx.x * win : dst;
+  const long long slots = win / nf;
+  if (mode <= 2) {
+    if (threadIdx.x == 0) {
+      for (int it = 0; it < iters; ++it) {
+        const long long slot = mode == 1 ? (it + blockIdx.x) % slots : it % slots;
+        float* d = base + slot * nf;
+        for (int off = 0; off < chunk_bytes; off += 16384) {
+          const int sz = min(16384, chunk_bytes - off);
+          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
+                           reinterpret_cast<char*>(d) + off),
+                       "r"(smem_u32(smem_raw + off)), "r"(sz)
+                       : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 8;" ::: "memory");
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+  } else {
+    for (int it = 0; it < iters; ++it) {
+      const long long slot = (it + blockIdx.x) % slots;
+      float* d = base + slot * nf;
+      for (int i = threadIdx.x * 4; i < nf; i += blockDim.x * 4) {
+        const float4 v = *reinterpret_cast<const float4*>(src + i);
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d + i), "f"(v.x), "f"(v.y), "f"(v.z),
+                     "f"(v.w)
+                     : "memory");
+      }
+    }
+  }
+}
+}  // namespace infcl
+
+extern "C" int infcl_diag_reduce_rate(float* dst, long long dst_floats, int chunk_bytes, int iters, int nblocks, int mode,
+                                      void* stream) {
+  if (!dst || chunk_bytes < 16 || chunk_bytes % 16 || chunk_bytes > 196608 || iters < 1 || nblocks < 1 || mode < 0 ||
+      mode > 3)
+    return -1;
+  const long long win = mode == 2 ? dst_floats / nblocks : dst_floats;
+  if (win < chunk_bytes / 4) return -2;
+  if (cudaFuncSetAttribute(infcl::probe_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, chunk_bytes) !=
+      cudaSuccess)
+    return -3;
+  infcl::probe_reduce_kernel<<<nblocks, 256, chunk_bytes, (cudaStream_t)stream>>>(dst, dst_floats, chunk_bytes, iters,
+                                                                                    mode);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+extern "C" const char* infcl_diag_last_error(void) { return infcl::last_error_string(); }

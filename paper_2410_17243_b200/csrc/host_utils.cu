@@ -3,7 +3,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -20,6 +22,8 @@ infcl_status fail(infcl_status st, const std::string& msg) {
   set_last_error(msg);
   return st;
 }
+
+const char* last_error_string() { return g_last_error.c_str(); }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -64,6 +68,15 @@ int num_sms() {
   }
   return n;
 }
+
+static thread_local int g_carve_pairs = 0;
+int max_pairs() {
+  int pairs = std::max(1, num_sms() / 2 - g_carve_pairs);
+  if (const char* e = getenv("INFCL_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(e)));  // diagnostic
+  return pairs;
+}
+PairCarveOut::PairCarveOut(int pairs) : saved(g_carve_pairs) { g_carve_pairs = std::max(0, pairs); }
+PairCarveOut::~PairCarveOut() { g_carve_pairs = saved; }
 
 }  // namespace infcl
 

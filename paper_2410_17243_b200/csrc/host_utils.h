@@ -13,6 +13,7 @@ namespace infcl {
 
 void set_last_error(const std::string& msg);
 infcl_status fail(infcl_status st, const std::string& msg);
+const char* last_error_string();  // this thread's detail (infcl_last_error / infcl_diag_last_error)
 
 #define INFCL_CUDA_TRY(expr)                                                                   \
   do {                                                                                         \
@@ -27,5 +28,13 @@ infcl_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, u
                             uint32_t box_cols, uint32_t box_rows);
 
 int num_sms();
+// CTA pairs the persistent pair kernels may occupy: num_sms() / 2, minus this thread's carve-out (SMs left free for
+// the NCCL ring transport's kernels, PairCarveOut), capped by INFCL_PAIRS (diagnostic)
+int max_pairs();
+struct PairCarveOut {  // RAII: leave `pairs` CTA pairs free while a ring call enqueues its kernels (this thread)
+  explicit PairCarveOut(int pairs);
+  ~PairCarveOut();
+  int saved;
+};
 
 }  // namespace infcl

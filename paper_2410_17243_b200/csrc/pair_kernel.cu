@@ -35,7 +35,7 @@ namespace infcl {
 // ---- optional per-launch event timing (infcl_profile_*)
 struct ProfState {
   bool on = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[2];
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[3];  // 0 fwd kernel, 1 bwd kernel, 2 ring block send
 };
 static ProfState& prof() {
   static ProfState p;
@@ -513,8 +513,7 @@ PassGeom pass_geom(int nrows, int ncols) {
   g.n_rb = (nrows + kRowsPerPair - 1) / kRowsPerPair;
   g.n_ct = (ncols + kColsPerTile - 1) / kColsPerTile;
   g.n_items = (long long)g.n_rb * g.n_ct;
-  int pairs = std::max(1, num_sms() / 2);
-  if (const char* e = getenv("INFCL_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(e)));  // diagnostic
+  const int pairs = max_pairs();
   g.npairs = (int)std::min<long long>(pairs, g.n_items);
   return g;
 }
@@ -652,7 +651,7 @@ void profile_enable(bool on) {
 }
 
 infcl_status profile_read(int kind, int* launches, double* total_ms) {
-  if (kind < 0 || kind > 1 || !launches || !total_ms) return fail(INFCL_ERR_INVALID_ARG, "bad profile query");
+  if (kind < 0 || kind > 2 || !launches || !total_ms) return fail(INFCL_ERR_INVALID_ARG, "bad profile query");
   double t = 0;
   for (auto& e : prof().ev[kind]) {
     INFCL_CUDA_TRY(cudaEventSynchronize(e.second));

@@ -260,8 +260,7 @@ PassGeom wide_geom(int nrows, int ncols) {
   g.n_rb = (nrows + kWRows - 1) / kWRows;
   g.n_ct = (ncols + kColsPerTile - 1) / kColsPerTile;
   g.n_items = (long long)g.n_rb * g.n_ct;
-  int pairs = std::max(1, num_sms() / 2);
-  if (const char* e = getenv("INFCL_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(e)));  // diagnostic
+  const int pairs = max_pairs();
   g.npairs = (int)std::min<long long>(pairs, g.n_items);
   return g;
 }

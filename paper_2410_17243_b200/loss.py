@@ -52,6 +52,7 @@ class RingComm:
     def __init__(self, group=None, device=None, transport: str = "nccl", max_b: int | None = None,
                  max_d: int | None = None, dtype=torch.bfloat16):
         import torch.distributed as dist
+        self.group = group  # the process group the ring (and every cross-rank reduction of this comm) spans
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.transport = transport
@@ -153,18 +154,26 @@ def infcl_backward(I_local, T_local, b: int, logit_scale: float, row_lse, col_ls
     return dI, dT
 
 
-def infcl_grad_scale(I_local, dI_local, logit_scale: float, group=None):
+def comm_sum(t: torch.Tensor, comm=None) -> torch.Tensor:
+    """Sum a per-rank partial over the ranks of ``comm``'s ring, in place: a no-op for a local loss (comm None or
+    world 1) -- never over an unrelated default process group (a DDP job computing a local loss must not add
+    other ranks' partials) -- and over the comm's own group otherwise."""
+    if comm is None or comm.world <= 1:
+        return t
+    import torch.distributed as dist
+    dist.all_reduce(t, group=comm.group)
+    return t
+
+
+def infcl_grad_scale(I_local, dI_local, logit_scale: float, comm=None):
     """g * dL/ds (learnable temperature): sum_i <dI_i, I_i> / s over the global batch (include/infcl.h).
-    The per-rank partial is summed with torch.distributed when a process group is initialised."""
+    The per-rank partial is summed over ``comm``'s ranks (the ring the loss was computed on), if any."""
     I_local = I_local.contiguous()
     dI_local = dI_local.contiguous()
     out = torch.empty((), device=I_local.device, dtype=torch.float64)
     L.call("infcl_grad_scale_partial", I_local.data_ptr(), dI_local.data_ptr(), _dtype_code(I_local),
            I_local.shape[0], I_local.shape[1], float(logit_scale), out.data_ptr(), _stream())
-    import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(out, group=group)
-    return out
+    return comm_sum(out, comm)
 
 
 def infcl_forward_virtual(I, T, logit_scale: float, world: int):
@@ -233,7 +242,7 @@ class _InfCLFunction(torch.autograd.Function):
         dI, dT = infcl_backward(I_local, T_local, b, s, r, c, dg, grad_out, rank, world, comm)
         ds = None
         if want_ds:  # g * dL/ds = sum_i <dI_i, I_i> / s over the global batch (include/infcl.h)
-            ds = infcl_grad_scale(I_local, dI, s).to(torch.float32)
+            ds = infcl_grad_scale(I_local, dI, s, comm).to(torch.float32)
         return dI.to(I_local.dtype), dT.to(T_local.dtype), ds, None, None, None, None, None
 
 

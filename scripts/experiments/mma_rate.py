@@ -9,7 +9,7 @@ for (M, N, amn, ncta, name) in [(128, 256, 0, 2, "S GEMM pair M128 N256 Kmaj"), 
                                 (128, 256, 0, 1, "1cta M128 N256"), (128, 128, 0, 1, "1cta M128 N128"),
                                 (128, 64, 0, 2, "pair M128 N64"), (256, 64, 1, 2, "pair M256 N64 MN")]:
     it = 4096
-    L.call("infcl_probe_mma_rate", M, N, amn, ncta, it, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    L.diag_call("infcl_probe_mma_rate", M, N, amn, ncta, it, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     c = out.cpu().tolist()
     flops_per_sm = 2 * M * N * 16 / ncta

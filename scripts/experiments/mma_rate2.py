@@ -7,7 +7,7 @@ for (M, N, amn, name) in [(128, 256, 0, "S pair M128N256"), (256, 128, 1, "dA pa
     for G in (0, 4, 8, 16):
         code = amn if G == 0 else (G << 1) | amn
         it = 4096
-        L.call("infcl_probe_mma_rate", M, N, code, 2, it, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        L.diag_call("infcl_probe_mma_rate", M, N, code, 2, it, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
         c = out.cpu().tolist()
         print(f"{name:22s} group={G:2d} total={c[1]/it:7.1f} cyc/mma -> {2*M*N*16/2/(c[1]/it):6.0f} flop/clk/SM")

@@ -8,7 +8,7 @@ for rep in range(2):
     for G in (0, 8):
         code = amn if G == 0 else (G << 1) | amn
         it = 8192
-        L.call("infcl_probe_mma_rate", M, N, code, 2, it, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        L.diag_call("infcl_probe_mma_rate", M, N, code, 2, it, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
         c = out.cpu().tolist()
         print(f"{name:22s} stage-group={G:2d} total={c[1]/it:7.1f} cyc/mma -> {2*M*N*16/2/(c[1]/it):6.0f} flop/clk/SM", flush=True)

@@ -35,11 +35,11 @@ def bwd():
 
 
 def rt_copy():  # plain cudaMemcpyAsync
-    assert K.L.lib().infcl_diag_copy(dst.data_ptr(), src.data_ptr(), src.numel(), 0, s2.cuda_stream) == 0
+    assert K.L.diag().infcl_diag_copy(dst.data_ptr(), src.data_ptr(), src.numel(), 0, s2.cuda_stream) == 0
 
 
 def ce_copy():  # cudaMemcpyBatchAsync + cudaMemcpyFlagPreferOverlapWithCompute (the IPC transport's copy)
-    assert K.L.lib().infcl_diag_copy(dst.data_ptr(), src.data_ptr(), src.numel(), 1, s2.cuda_stream) == 0
+    assert K.L.diag().infcl_diag_copy(dst.data_ptr(), src.data_ptr(), src.numel(), 1, s2.cuda_stream) == 0
 
 
 def sm_copy():

@@ -3,16 +3,30 @@ host-only entry points behave; device entry points fail loudly (no CPU fallback)
 import ctypes
 import os
 import re
+import shutil
+import subprocess
+
+import pytest
 
 from paper_2410_17243_b200 import _lib as L
 
-HEADER = os.path.join(os.path.dirname(__file__), "..", "include", "infcl.h")
+INCLUDE = os.path.join(os.path.dirname(__file__), "..", "include")
+HEADER = os.path.join(INCLUDE, "infcl.h")
+DIAG_HEADER = os.path.join(INCLUDE, "infcl_diag.h")
 
 
-def declared_symbols():
-    src = open(HEADER).read()
+def declared_symbols(path=HEADER):
+    src = open(path).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(infcl_[a-z0-9_]+)\s*\(", src)))
+
+
+def exported_symbols(so):
+    """Defined dynamic symbols of a shared library (nm -D), i.e. everything a dlsym can reach."""
+    if not shutil.which("nm"):
+        pytest.skip("nm not available")
+    out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True, check=True).stdout
+    return sorted({ln.split()[-1] for ln in out.splitlines() if ln.strip() and ln.split()[-2] in "TtDdBbRrWwVv"})
 
 
 def test_header_symbols_exported():
@@ -23,6 +37,22 @@ def test_header_symbols_exported():
         assert hasattr(lib, n), n
         assert n in L.SIGNATURES, f"binding lacks {n}"
     assert set(L.SIGNATURES) == set(names)
+
+
+def test_product_exports_exactly_the_header():
+    """libinfcl.so exports the symbols include/infcl.h declares and nothing else (no undeclared entry points,
+    no C++ internals, no probes: those live in libinfcl_diag.so)."""
+    assert exported_symbols(L.LIB_PATH) == declared_symbols()
+
+
+def test_diag_library_exports_exactly_its_header():
+    names = declared_symbols(DIAG_HEADER)
+    assert exported_symbols(L.DIAG_PATH) == names
+    assert set(L.DIAG_SIGNATURES) == set(names)
+    assert not set(names) & set(declared_symbols())  # disjoint from the product ABI
+    D = L.diag()
+    for n in names:
+        assert hasattr(D, n), n
 
 
 def test_host_functions():

@@ -111,20 +111,26 @@ def test_cfg3_codebook_closed_form():
     assert rel_norm(dT.cpu().numpy()[rows], cf["dT"]) <= 2e-3
 
 
-@pytest.mark.parametrize("b,d", [(32768, 128), (40000, 64)])
+def e2e_boundaries(b):
+    """Row / column boundaries of infcl_loss_grad_host's pipelined schedule (api.cu: forward I chunks at
+    sixteenths {1, 4, 10}, dT-pass chunks at {6, 11, 15}, 128-row aligned; T split at 3/8, 256 aligned)."""
+    at16 = [min(b, (b * e // 16 + 127) // 128 * 128) for e in (1, 4, 6, 10, 11, 15)]
+    return at16 + [min(b, (b * 3 // 8 + 255) // 256 * 256)]
+
+
+@pytest.mark.parametrize("b,d", [(32768, 128), (40000, 64), (65536, 512)])
 def test_e2e_host_entry_chunked(b, d):
     """Host end-to-end entry at sizes where it pipelines PCIe copies against row chunks of the forward and of
-    the dT pass (4 chunks; b = 40000 leaves a ragged last chunk): loss and stratified gradient rows against
-    the fp64 oracle (streamed r, c; sampled rows of dI and dT)."""
+    the dT pass (b = 40000 leaves ragged chunks; b = 65536, d = 512 is cfg2, the shape bench.py's e2e times):
+    the loss against the streamed fp64 oracle and stratified gradient rows plus
+    the rows on both sides of every chunk / piece boundary against the exact fp64 rows."""
     I, T = make_features(b, d, seed=11, dist="paired")
     loss, dI, dT = K.infcl_loss_grad_host(I.pin_memory(), T.pin_memory(), S)
     ref = oracle.streamed_forward(I, T, S, chunk=4096)
     assert abs(loss.item() - ref["loss"]) <= 1e-4 * abs(ref["loss"])
     rows = stratified_rows(b, 96)
-    # block / chunk boundaries (eighths of b, 128-aligned; T halves) are in the sample
-    cuts = [min(b, (b * e // 8 + 127) // 128 * 128) for e in range(1, 8)]
-    rows = np.unique(np.concatenate([rows, [x for c in cuts for x in (c - 1, c)]]))
-    rows = rows[rows < b]
+    rows = np.unique(np.concatenate([rows, [x for c in e2e_boundaries(b) for x in (c - 1, c)]]))
+    rows = rows[(rows >= 0) & (rows < b)]
     rdI = oracle.sampled_row_grads(I, T, S, ref["r"], ref["c"], rows)
     rdT = oracle.sampled_row_grads(T, I, S, ref["c"], ref["r"], rows)
     assert rel_norm(dI.numpy()[rows], rdI) <= 2e-3

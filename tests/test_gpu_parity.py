@@ -20,9 +20,8 @@ LOSS_RTOL = 1e-4
 GRAD_RTOL = 2e-3
 LSE_ATOL = 2e-3
 # the north star's relative loss gate is undefined at L ~ 0, so an absolute floor of
-# 2^-20 max(1, s) (a few fp32 ulps of a logit of magnitude s) is added; the gradient gate adds the rounding
-# term u_G * ||s |G| |B|||, u_G = 2^-8 (bf16 G), which only matters for ill-conditioned (cancelling) gradients.
-U_G = 2.0 ** -8
+# 2^-20 max(1, s) (a few fp32 ulps of a logit of magnitude s) is added.  Gradient gates are the plain north-star
+# normwise 2e-3 (no conditioning term): every gate below rejects an all-zero gradient (grad_ok asserts it).
 
 
 def loss_ok(got, ref, s):
@@ -34,6 +33,17 @@ def rel_norm(got, ref):
     ref = np.asarray(ref, dtype=np.float64)
     nr = np.linalg.norm(ref)
     return np.linalg.norm(got - ref) / nr if nr > 0 else np.linalg.norm(got - ref)
+
+
+def grad_ok(got, want, rtol=GRAD_RTOL):
+    """North-star gradient gate ||got - want|| <= rtol ||want||; checks the gate itself is not vacuous (an all-zero
+    gradient fails it)."""
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    tol = rtol * np.linalg.norm(want)
+    assert np.linalg.norm(want) > tol  # zero fails this gate
+    err = np.linalg.norm(got - want)
+    assert err <= tol, (err / np.linalg.norm(want), rtol)
 
 
 def check_all(I, T, s, g=1.0, world=None, want_grads=True):
@@ -63,8 +73,8 @@ def check_all(I, T, s, g=1.0, world=None, want_grads=True):
         got = got.cpu().numpy()
         assert np.isfinite(got).all()
         if np.linalg.norm(want) > 1e-9:
-            assert rel_norm(got, want) <= GRAD_RTOL, rel_norm(got, want)
-        else:
+            grad_ok(got, want)
+        else:  # identical features / s = 0: the exact gradient is 0
             assert np.abs(got).max() <= 1e-6 * max(s, 1.0) * abs(g)
 
 
@@ -100,23 +110,45 @@ def test_identical_features_log_b():
     check_all(I, T, 14.2857)
 
 
-@pytest.mark.parametrize("s", [1.0, 14.2857])
+@pytest.mark.parametrize("s", [1.0, 3.0])
 def test_onehot_closed_form_gpu(s):
-    """Closed form (oracle.onehot_closed_form).  At s=14.3 the own-class gradient component is
-    s g/b (m p - 1) with m p - 1 ~ -2e-5: a cancellation of O(1) summands that no bf16-G evaluation resolves,
-    so the gate there includes the u_G * ||s|G||T||| conditioning term (DESIGN.md Tolerances)."""
+    """Closed form (oracle.onehot_closed_form, pinned in tests/test_oracle_pins.py): loss, r, c and the full
+    gradients at the plain north-star gates.  At s <= 3 the own-class component s g/b (m p - 1) is O(1)
+    (m p - 1 = -0.97 at s = 1, -0.61 at s = 3): no cancellation, every component is well conditioned."""
     b, K_, d = 1024, 32, 64
     I, T = make_features(b, d, dist="onehot", K=K_)
     cf = oracle.onehot_closed_form(b, K_, d, s)
     loss, r, c, dg = K.infcl_forward(I.cuda(), T.cuda(), b, s)
     dI, dT = K.infcl_backward(I.cuda(), T.cuda(), b, s, r, c, dg, torch.tensor(1.0, device="cuda"))
     assert loss_ok(loss.item(), cf["loss"], s)
-    aI, aT = oracle.backward_abs(I, T, s)
-    for got, want, a in ((dI, cf["dI"], aI), (dT, cf["dT"], aT)):
-        err = np.linalg.norm(got.cpu().numpy() - want)
-        if s <= 1.0:
-            assert err <= GRAD_RTOL * np.linalg.norm(want)
-        assert err <= GRAD_RTOL * np.linalg.norm(want) + U_G * np.linalg.norm(a)
+    assert np.abs(r.cpu().numpy() - cf["r"]).max() <= LSE_ATOL and np.abs(c.cpu().numpy() - cf["c"]).max() <= LSE_ATOL
+    grad_ok(dI.cpu().numpy(), cf["dI"])
+    grad_ok(dT.cpu().numpy(), cf["dT"])
+
+
+def test_onehot_closed_form_gpu_large_scale():
+    """s = 14.2857 (the CLIP init): loss, r, c at the north-star gates.  The own-class gradient component is
+    s g/b (m p - 1) with m p - 1 = -1.9e-5, the difference of O(1) summands (the exact fp32 diagonal term and
+    m - 1 identical bf16-rounded G entries, DESIGN.md Tolerances), which no 16-bit G resolves; it is not gated.
+    The off-class components s g m q / b (Eq.7, q = e^{-Lambda}) are sums of m same-signed terms:
+    each is gated ELEMENTWISE at 2e-3 relative, and the components outside the K class directions are exactly 0."""
+    b, K_, d, s = 1024, 32, 64, 14.2857
+    I, T = make_features(b, d, dist="onehot", K=K_)
+    cf = oracle.onehot_closed_form(b, K_, d, s)
+    loss, r, c, dg = K.infcl_forward(I.cuda(), T.cuda(), b, s)
+    dI, dT = K.infcl_backward(I.cuda(), T.cuda(), b, s, r, c, dg, torch.tensor(1.0, device="cuda"))
+    assert loss_ok(loss.item(), cf["loss"], s)
+    assert np.abs(r.cpu().numpy() - cf["r"]).max() <= LSE_ATOL and np.abs(c.cpu().numpy() - cf["c"]).max() <= LSE_ATOL
+    own = np.zeros((b, d), dtype=bool)
+    own[np.arange(b), np.arange(b) % K_] = True
+    off = np.zeros((b, d), dtype=bool)
+    off[:, :K_] = True
+    off &= ~own
+    for got, want in ((dI.cpu().numpy().astype(np.float64), cf["dI"]), (dT.cpu().numpy().astype(np.float64), cf["dT"])):
+        w = want[off]
+        assert np.all(np.abs(w) > 0)
+        assert np.max(np.abs(got[off] - w) / np.abs(w)) <= GRAD_RTOL
+        assert np.all(got[:, K_:] == 0.0)
 
 
 def test_fp32_cfg1():
@@ -160,8 +192,9 @@ def test_autograd_function():
     loss = K.infcl_loss(Id, Td, 14.2857)
     (2.0 * loss).backward()
     rdI, rdT = oracle.backward(I, T, 14.2857, 2.0)
-    assert rel_norm(Id.grad.float().cpu().numpy(), rdI) < 1e-2  # bf16-rounded gradient
-    assert rel_norm(Td.grad.float().cpu().numpy(), rdT) < 1e-2
+    # the autograd gradients come back in the inputs' dtype (bf16): the gate adds bf16's unit roundoff 2^-8
+    grad_ok(Id.grad.float().cpu().numpy(), rdI, GRAD_RTOL + 2.0 ** -8)
+    grad_ok(Td.grad.float().cpu().numpy(), rdT, GRAD_RTOL + 2.0 ** -8)
 
 
 def test_e2e_host_entry():
@@ -169,7 +202,8 @@ def test_e2e_host_entry():
     loss, dI, dT = K.infcl_loss_grad_host(I, T, 14.2857)
     ref = oracle.loss_and_grads(I, T, 14.2857)
     assert loss_ok(loss.item(), ref["loss"], 14.2857)
-    assert rel_norm(dI.numpy(), ref["dI"]) <= GRAD_RTOL and rel_norm(dT.numpy(), ref["dT"]) <= GRAD_RTOL
+    grad_ok(dI.numpy(), ref["dI"])
+    grad_ok(dT.numpy(), ref["dT"])
 
 
 def test_nan_propagates():
@@ -210,23 +244,25 @@ def test_forward_exact_fallback_adversarial_columns():
 
 
 @pytest.mark.parametrize("s", [1.0, 14.2857, 100.0])
-def test_grad_scale(s):
-    """g dL/ds via the bilinearity identity s dL/ds = sum_i <dI_i, I_i> against the oracle's direct
-    sum_ij G_ij <I_i, T_j>."""
-    b, d = 2048, 256
+def test_grad_scale_cfg2(s):
+    """g dL/ds at cfg2's size (b = 65536, d = 512, random paired inputs) through
+    infcl_grad_scale (s dL/ds = sum_i <dI_i, I_i>) against the exact fp64 oracle sum_ij G_ij <I_i, T_j>
+    (oracle.streamed_grad_scale with the exact streamed LSEs): |ds - ref| <= 2e-3 |ref| + 1e-30.  At s = 1 and
+    14.3 ds ~ -0.7 / -0.1 is dominated by the exact fp32 diagonal term; at s = 100 the diagonal term vanishes
+    (P_ii = 1 in fp32) and ds ~ 5e-24 is a sum of same-signed off-diagonal terms -- no cancellation at any s, so
+    the same relative gate applies, and it rejects ds = 0."""
+    b, d, g = 65536, 512, 0.7
     I, T = make_features(b, d, seed=13, dist="paired")
     Id, Td = I.cuda(), T.cuda()
     loss, r, c, dg = K.infcl_forward(Id, Td, b, s)
-    dI, dT = K.infcl_backward(Id, Td, b, s, r, c, dg, torch.tensor(0.7, device="cuda"))
+    dI, dT = K.infcl_backward(Id, Td, b, s, r, c, dg, torch.tensor(g, device="cuda"))
     ds = K.infcl_grad_scale(Id, dI, s).item()
-    _, _, ref = oracle.backward(I, T, s, 0.7, want_ds=True)
-    aI, _ = oracle.backward_abs(I, T, s, 0.7)
-    # |d ds| <= |sum_i <d dI_i, I_i>| / s <= ||d dI|| ||I|| / s: gate from the gradient gate
-    # gradient gate incl. its absolute floor 1e-6 max(s,1)|g| per element (check_all), mapped through |<dI, I>| / s
-    dI_err = GRAD_RTOL * np.linalg.norm(oracle.backward(I, T, s, 0.7)[0]) + U_G * np.linalg.norm(aI) \
-        + 1e-6 * max(s, 1.0) * 0.7 * np.sqrt(b * d)
-    tol = dI_err * np.linalg.norm(oracle.to_f64(I)) / s
-    assert abs(ds - ref) <= tol, (ds, ref, tol)
+    del dI, dT
+    f = oracle.streamed_forward(I, T, s, chunk=2048)
+    ref = oracle.streamed_grad_scale(I, T, s, f["r"], f["c"], g)
+    tol = 2e-3 * abs(ref) + 1e-30
+    assert abs(ref) > tol
+    assert abs(ds - ref) <= tol, (ds, ref, abs(ds - ref) / abs(ref))
 
 
 def test_autograd_learnable_scale():

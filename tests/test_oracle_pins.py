@@ -163,6 +163,24 @@ def test_scale_identity(s):
     assert ds == pytest.approx(fd, rel=1e-6, abs=1e-9)
 
 
+@pytest.mark.parametrize("s", [1.0, 14.2857, 100.0])
+def test_streamed_grad_scale(s):
+    """streamed_grad_scale (the large-b ds oracle) against central finite differences of the brute-force loss
+    (tests/brute.py, Eq.1 written out) and the s dL/ds = sum_i <dI_i, I_i> identity, across chunkings."""
+    b, d = 20, 8
+    I = rand_feats(b, d, 23)
+    T = rand_feats(b, d, 24)
+    s32 = float(np.float32(s))
+    f = O.forward(I, T, s)
+    h = 1e-5 * max(1.0, s32)
+    fd = (brute.loss(I.tolist(), T.tolist(), s32 + h) - brute.loss(I.tolist(), T.tolist(), s32 - h)) / (2 * h)
+    dI, _ = O.backward(I, T, s, 0.7)
+    for chunk in (1, 7, 64):
+        ds = O.streamed_grad_scale(I, T, s, f["r"], f["c"], 0.7, chunk=chunk)
+        assert ds == pytest.approx(0.7 * fd, rel=1e-6, abs=1e-9)
+        assert s32 * ds == pytest.approx((dI * I).sum(), rel=1e-10, abs=1e-13)
+
+
 def test_swap_symmetry():
     b, d = 40, 12
     I = rand_feats(b, d, 31)

@@ -141,3 +141,26 @@ def _bench_reduce_worker(rank, world, port, q):
 def test_bench_max_over_ranks_gloo():
     res = _run(_bench_reduce_worker, 2, timeout=120)
     assert res == [(0, 3.0), (1, 3.0)]
+
+
+def _comm_sum_worker(rank, world, port, q):
+    _init(rank, world, port)
+    try:
+        from types import SimpleNamespace
+        from paper_2410_17243_b200.loss import comm_sum
+        sub = [dist.new_group([0, 1]), dist.new_group([2, 3])]  # every rank creates every group
+        mine = sub[rank // 2]
+        x = torch.tensor(float(rank + 1), dtype=torch.float64)
+        local = comm_sum(x.clone(), None)  # local loss in a multi-rank job: no reduction
+        one = comm_sum(x.clone(), SimpleNamespace(world=1, group=None))
+        ring = comm_sum(x.clone(), SimpleNamespace(world=2, group=mine))  # ring on a subgroup: that group only
+        q.put((rank, float(local), float(one), float(ring)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_grad_scale_reduction_scope_gloo():
+    """g dL/ds partials are summed over the loss's own ring group only -- not over the default group
+    when the loss is local (comm None / world 1), and over a subgroup when the ring spans one."""
+    res = _run(_comm_sum_worker, 4, timeout=120)
+    assert res == [(0, 1.0, 1.0, 3.0), (1, 2.0, 2.0, 3.0), (2, 3.0, 3.0, 7.0), (3, 4.0, 4.0, 7.0)]
