@@ -35,3 +35,4 @@ from .infonce import (  # noqa: F401
     codebook_closed_form,
     to_f64,
 )
+from . import ntxent  # noqa: F401  (SimCLR NT-Xent, the second workload: SURVEY 8(f) f4)

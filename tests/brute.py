@@ -40,3 +40,37 @@ def fd_grads(I, T, s, h=1e-6):
                 M[i][k] = v
                 D[i][k] = (lp - lm) / (2 * h)
     return dI, dT
+
+
+def ntxent_loss(A, B, s):
+    """NT-Xent written from its definition (SimCLR; oracle/ntxent.py readings N1-N3) with Python loops: views
+    z = A + B (2b), each view's positive is the other view of its example, its own similarity is excluded."""
+    z = [list(r) for r in A] + [list(r) for r in B]
+    n = len(z)
+    b = n // 2
+    tot = []
+    for k in range(n):
+        row = [s * dot(z[k], z[j]) for j in range(n) if j != k]
+        m = max(row)
+        lse = m + math.log(math.fsum(math.exp(v - m) for v in row))
+        tot.append(lse - s * dot(z[k], z[(k + b) % n]))
+    return math.fsum(tot) / n
+
+
+def ntxent_fd_grads(A, B, s, h=1e-6):
+    A = [list(map(float, r)) for r in A]
+    B = [list(map(float, r)) for r in B]
+    out = []
+    for M in (A, B):
+        D = [[0.0] * len(M[0]) for _ in M]
+        for i in range(len(M)):
+            for k in range(len(M[0])):
+                v = M[i][k]
+                M[i][k] = v + h
+                lp = ntxent_loss(A, B, s)
+                M[i][k] = v - h
+                lm = ntxent_loss(A, B, s)
+                M[i][k] = v
+                D[i][k] = (lp - lm) / (2 * h)
+        out.append(D)
+    return out
