@@ -353,6 +353,7 @@ def run_ours(args):
 
     # end-to-end through the public API with host buffers
     e2e = run_e2e(args, K, b, d, bs, s, rank, world, comm, dev)
+    ntx = run_ntxent(args, K, b, d, s, dev, flush) if world == 1 and not args.no_ntxent else None
 
     out = None
     if rank == 0:
@@ -372,12 +373,48 @@ def run_ours(args):
                "gpu_launches": launches, "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cb, "e2e": e2e}
         if ring is not None:
             out["ring"] = ring
+        if ntx is not None:
+            out["second_workload"] = ntx
         print(json.dumps(out), flush=True)
     if comm is not None:
         comm.close()
     if world > 1:
         dist.destroy_process_group()
     return out
+
+
+def run_ntxent(args, K, b, d, s, dev, flush):
+    """The second workload: NT-Xent (SimCLR) over the same number of views as the headline
+    workload (b/2 examples x 2 views, d), device-resident, CUDA events per step, L2 flushed between steps."""
+    from synth import make_features_device
+    bx = b // 2
+    A, B = make_features_device(bx, d, seed=args.seed * 1000 + 7, device=dev)
+    ws = K.alloc_workspace(bx, d, 1, torch.bfloat16, dev)
+    g = torch.ones((), device=dev)
+
+    def step():
+        loss, la, lb, pos = K.ntxent_forward(A, B, bx, s, workspace=ws)
+        return K.ntxent_backward(A, B, bx, s, la, lb, pos, g, workspace=ws)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    n = max(3, min(args.steps, 10))
+    ts = []
+    for _ in range(n):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.mean(ts)
+    # executed work: forward 3 b_x^2 blocks (2 b_x^2 d each), backward 4 block passes (4 b_x^2 d each)
+    flop = (3 * 2 + 4 * 4) * float(bx) * bx * d
+    return {"workload": f"NT-Xent (SimCLR) over {2 * bx} views: {bx} examples x 2, d={d}, bf16",
+            "metric": "loss fwd+bwd views/s", "value": 2 * bx / (ms / 1e3), "ms_per_step": ms, "steps": n,
+            "executed_tflops": flop / (ms / 1e3) / 1e12}
 
 
 def run_e2e(args, K, b, d, bs, s, rank, world, comm, dev):
@@ -437,6 +474,7 @@ def main(argv=None):
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ntxent", action="store_true", help="skip the second-workload (NT-Xent) line")
     ap.add_argument("--transport", choices=["ipc", "nccl"], default="ipc",
                     help="ring transport for N>1: copy-engine writes over CUDA IPC peer memory (default) or NCCL P2P")
     args = ap.parse_args(argv)

@@ -139,6 +139,29 @@ infcl_status infcl_backward(infcl_comm comm, const void* I_local, const void* T_
                             float* dT_local, void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------------------------
+ * infcl_ntxent_forward / infcl_ntxent_backward -- the single-modality NT-Xent loss (SimCLR; self-supervised
+ * learning is the paper's second named application), on the same kernels.
+ * Views: A_local, B_local [b/world][d] bf16 (the two augmented views of this rank's examples; rank r owns
+ * examples [r*b/world, (r+1)*b/world)); b = GLOBAL number of examples (2b views).  With Z = [A; B] and
+ * x_kk' = s <z_k, z_k'>, every view's positive is the other view of its example and its own similarity is
+ * excluded (oracle/ntxent.py readings N1-N3):
+ *   lse_a[i], lse_b[i] = LSE over the 2b - 1 other views of A_i, B_i   (out, fp32 [b/world])
+ *   pos[i]             = x(A_i, B_i) = s <A_i, B_i>                       (out, fp32 [b/world])
+ *   loss               = (1/2b) sum over all 2b views of (lse - pos)       (out, device fp32 scalar, every rank)
+ *   dA, dB             = g dL/dA, g dL/dB for this rank's examples        (out, fp32 [b/world][d], overwritten)
+ * The 2b x 2b similarity runs as four b x b blocks: (A, B) is the CLIP pair (positives on its diagonal), (A, A)
+ * and (B, B) are self-masked; at world > 1 each block is a ring over `comm` (collective, as infcl_forward).
+ * Workspace: infcl_comm_workspace_bytes(comm, b, d, world, INFCL_BF16).  fp32 views: INFCL_ERR_UNSUPPORTED.
+ * ------------------------------------------------------------------------------------------------- */
+infcl_status infcl_ntxent_forward(infcl_comm comm, const void* A_local, const void* B_local, infcl_dtype dt, int64_t b,
+                                  int d, float logit_scale, int rank, int world, float* lse_a, float* lse_b,
+                                  float* pos, float* loss, void* workspace, size_t ws_bytes, void* stream);
+infcl_status infcl_ntxent_backward(infcl_comm comm, const void* A_local, const void* B_local, infcl_dtype dt,
+                                   int64_t b, int d, float logit_scale, int rank, int world, const float* lse_a,
+                                   const float* lse_b, const float* pos, const float* grad_loss, float* dA_local,
+                                   float* dB_local, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------------
  * infcl_grad_scale_partial -- g * dL/ds for a learnable logit scale (temperature, the
  * CLIP convention of P:91's omitted temperature).  x_ij = s <I_i, T_j> is bilinear, so over the global batch
  * s * dL/ds = sum_i <dI_i, I_i> exactly (pinned: tests/test_oracle_pins.py::test_scale_identity).

@@ -47,6 +47,8 @@ SIGNATURES = {
     "infcl_forward_virtual": (_i, [_p, _p, _i, _i64, _i, _f, _i, _p, _p, _p, _p, _p, _sz, _p]),
     "infcl_backward_virtual": (_i, [_p, _p, _i, _i64, _i, _f, _i, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "infcl_grad_scale_partial": (_i, [_p, _p, _i, _i64, _i, _f, _p, _p]),
+    "infcl_ntxent_forward": (_i, [_p, _p, _p, _i, _i64, _i, _f, _i, _i, _p, _p, _p, _p, _p, _sz, _p]),
+    "infcl_ntxent_backward": (_i, [_p, _p, _p, _i, _i64, _i, _f, _i, _i, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "infcl_e2e_scratch_bytes": (_sz, [_i64, _i, _i]),
     "infcl_loss_grad_host": (_i, [_p, _p, _i, _i64, _i, _f, _f, _p, _p, _p, _p, _sz, _p]),
     "infcl_ring_block": (_i, [_i, _i, _i]),

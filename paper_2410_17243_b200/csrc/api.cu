@@ -308,7 +308,7 @@ struct Layout {
   PassGeom g{};
   long long slot_ld = 0;
   size_t off_slots, off_rparts, off_rstate, off_cstate, off_own2, off_ring_lse, off_ring_blk, off_expA, off_expB,
-      off_dscr, off_tails, off_acc, total;
+      off_dscr, off_tails, off_xstate, off_acc, total;
 };
 
 // ring_ws: the ring's receive buffers live in the workspace (NCCL transport); the IPC transport receives
@@ -344,6 +344,8 @@ Layout make_layout(int64_t b, int d, int world, infcl_dtype dt, bool ring_ws = t
   // backward: per-pair partials of split tail row blocks (< 2P slots of 128 rows x dk fp32; any row range of the
   // pass has at most P - 1 tail row blocks), combined in pair order -> deterministic gradients
   L.off_tails = take((size_t)(2 * L.g.npairs - 1) * kRowsPerPair * L.dk * sizeof(float));
+  // NT-Xent (infcl_ntxent_*): the travelling (unused) column state of the self-similarity rings
+  L.off_xstate = take((size_t)L.bs * sizeof(float2));
   L.off_acc = take(64);
   L.total = o;
   return L;
@@ -395,6 +397,7 @@ struct Rank {
   float* dscr() const { return reinterpret_cast<float*>(ws + L.off_dscr); }
   double* acc() const { return reinterpret_cast<double*>(ws + L.off_acc); }
   float* tails() const { return reinterpret_cast<float*>(ws + L.off_tails); }
+  float2* xstate(int i) const { return reinterpret_cast<float2*>(ws + L.off_xstate) + (size_t)i * L.bs; }
 };
 
 infcl_status prepare_rank(Rank& R, const void* I, const void* T, infcl_dtype dt, int64_t b, int d, float s, int world,
@@ -456,14 +459,16 @@ void fwd_finish(Rank& R, const float2* own_cstate, float* row_lse, float* col_ls
 
 // ---- backward pieces
 infcl_status bwd_step(Rank& R, const __nv_bfloat16* rowsA, const float* lse_rows2, const __nv_bfloat16* held,
-                      const float* lse_cols2, bool own, float* dst, int ld_dst, const float* grad, cudaStream_t st) {
+                      const float* lse_cols2, bool own, float* dst, int ld_dst, const float* grad, cudaStream_t st,
+                      bool self_mask = false) {
   PassArgs a{};
   a.A = rowsA;
   a.B = held;
   a.nrows = a.ncols = R.L.bs;
   a.dk = a.ld = R.L.dk;
   a.scale = R.s;
-  a.diag_on = own ? 1 : 0;
+  a.diag_on = own && !self_mask ? 1 : 0;
+  a.self_mask = own && self_mask ? 1 : 0;
   a.lse_row2 = lse_rows2;
   a.lse_col2 = lse_cols2;
   a.dA = dst;
@@ -815,7 +820,9 @@ infcl_status run_ring(infcl_comm c, const std::vector<ROp>& ops, RingCtx& x, cud
       case OP_COMPUTE: TRY(x.compute(op.c, ptr(op.a), op.b == BUF_NONE ? nullptr : ptr(op.b))); break;
       case OP_MERGE: x.merge(static_cast<float2*>(ptr(op.a))); break;
       case OP_FINISH: x.finish(static_cast<const float2*>(ptr(op.a))); break;
-      case OP_ALLRED: TRY(allreduce_acc(c, x.acc)); break;
+      case OP_ALLRED:
+        if (x.acc) TRY(allreduce_acc(c, x.acc));  // NT-Xent's self-similarity rings reduce nothing
+        break;
       default: return fail(INFCL_ERR_INVALID_ARG, "bad ring op");
     }
   }
@@ -1022,6 +1029,157 @@ extern "C" infcl_status infcl_backward(infcl_comm comm, const void* I_local, con
                                        float* dT, void* ws, size_t ws_bytes, void* stream) {
   return backward_impl(comm, I_local, T_local, dt, b, d, s, rank, world, row_lse, col_lse, diag, grad, dI, dT, ws,
                        ws_bytes, stream, nullptr);
+}
+
+// ------------------------------------------------------------------------------------------ NT-Xent (SimCLR)
+// The second workload through the same kernels (oracle/ntxent.py readings N1-N4).  With views
+// Z = [A; B] the 2b x 2b similarity splits into four b x b blocks: (A, B) and its transpose hold the positives on
+// their diagonal -- exactly the CLIP pair (I, T) = (A, B) -- and (A, A), (B, B) hold the self-similarities on
+// theirs, excluded by self-masked launches.  Row LSEs: r_A over the rows of (A, B) and (A, A); r_B over the
+// columns of (A, B) and the rows of (B, B) (the (B, B) row state seeds the column state the (A, B) pass
+// accumulates into).  Loss: the CLIP expression with (r, c) = (r_A, r_B) and the same b.  Gradients: dA = the CLIP
+// dI with (r, c) = (r_A, r_B) plus the self-masked pass (rows A, streamed A, LSE r_A on both sides); dB likewise.
+// At world > 1 every block is a ring over the ranks with the same schedule (fwd_ring_ops / bwd_ring_ops).
+namespace {
+// self-similarity forward block: rows vs held views of the same side, the own block self-masked; row partials
+// merged into `rstate` (the column statistics are those of the rows, by symmetry, and are not used)
+infcl_status fwd_self_step(Rank& R, const __nv_bfloat16* rows, const __nv_bfloat16* held, bool own, float2* rstate,
+                           cudaStream_t st) {
+  PassArgs a{};
+  a.A = rows;
+  a.B = held;
+  a.nrows = a.ncols = R.L.bs;
+  a.dk = a.ld = R.L.dk;
+  a.scale = R.s;
+  a.self_mask = own ? 1 : 0;
+  a.col_slots = R.slots();
+  a.slot_ld = R.L.slot_ld;
+  a.row_parts = R.rparts();
+  TRY(launch_pair_forward(a, st));
+  launch_merge_rows(R.rparts(), rstate, R.L.bs, fwd_geom(R.L.bs, R.L.bs), st);
+  return INFCL_OK;
+}
+
+infcl_status ntxent_check(infcl_dtype dt, int world, infcl_comm comm) {
+  if (dt != INFCL_BF16) return fail(INFCL_ERR_UNSUPPORTED, "NT-Xent takes bf16 views");
+  if (world > 1 && !comm) return fail(INFCL_ERR_CONFIG, "world > 1 needs a communicator");
+  return INFCL_OK;
+}
+
+// one self-similarity ring (world > 1): rows stationary, the same side's block travelling
+infcl_status fwd_self_ring(infcl_comm comm, Rank& R, int rank, int world, const __nv_bfloat16* rows,
+                           float2* rstate, cudaStream_t st) {
+  std::vector<ROp> ops;
+  fwd_ring_ops(world, rank, ops);
+  launch_init_state(R.xstate(0), R.L.bs, st);
+  RingCtx x;
+  x.own = rows;
+  x.owncs = R.xstate(0);
+  x.bytes[XK_BLK] = (size_t)R.L.bs * R.L.dk * 2;
+  x.bytes[XK_CS] = (size_t)R.L.bs * sizeof(float2);
+  x.compute = [&](int k, const void* blk, const void*) {
+    return fwd_self_step(R, rows, static_cast<const __nv_bfloat16*>(blk), k == 0, rstate, st);
+  };
+  x.merge = [](float2*) {};
+  x.finish = [](const float2*) {};
+  return run_ring(comm, ops, x, st);
+}
+}  // namespace
+
+extern "C" infcl_status infcl_ntxent_forward(infcl_comm comm, const void* A_local, const void* B_local, infcl_dtype dt,
+                                             int64_t b, int d, float s, int rank, int world, float* lse_a,
+                                             float* lse_b, float* pos, float* loss, void* ws, size_t ws_bytes,
+                                             void* stream) {
+  const size_t need = infcl_comm_workspace_bytes(world > 1 ? comm : nullptr, b, d, world, dt);
+  TRY(validate(A_local, B_local, dt, b, d, s, rank, world, ws, ws_bytes, need));
+  TRY(ntxent_check(dt, world, comm));
+  if (!lse_a || !lse_b || !pos || !loss) return fail(INFCL_ERR_INVALID_ARG, "null output pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PairCarveOut carve(ring_carveout(comm, world));
+  Rank R;
+  TRY(prepare_rank(R, A_local, B_local, dt, b, d, s, world, ws, st, world == 1 || ring_in_ws(comm)));
+  if (world > 1) TRY(ring_setup(comm, R, rank, world));
+  INFCL_CUDA_TRY(cudaMemsetAsync(R.acc(), 0, sizeof(double), st));
+  TRY(fwd_begin(R, st));  // rstate: A views' rows; cstate(0): B views' rows
+  if (world == 1) {
+    TRY(fwd_self_step(R, R.B, R.B, true, R.cstate(0), st));  // (B, B)
+    TRY(fwd_self_step(R, R.A, R.A, true, R.rstate(), st));   // (A, A)
+    TRY(fwd_step_main(R, R.B, true, pos, st));                // (A, B): positives
+    fwd_step_merge(R, R.cstate(0), st);
+    fwd_finish(R, R.cstate(0), lse_a, lse_b, pos, R.acc(), st);
+    launch_loss_write(R.acc(), loss, b, st);
+    INFCL_CUDA_TRY(cudaGetLastError());
+    return INFCL_OK;
+  }
+  // the (B, B) ring seeds the B rows' state, which then travels as the (A, B) ring's own column state
+  TRY(fwd_self_ring(comm, R, rank, world, R.B, R.cstate(0), st));
+  TRY(fwd_self_ring(comm, R, rank, world, R.A, R.rstate(), st));
+  std::vector<ROp> ops;
+  fwd_ring_ops(world, rank, ops);
+  RingCtx x;
+  x.own = R.B;
+  x.owncs = R.cstate(0);
+  x.bytes[XK_BLK] = (size_t)R.L.bs * R.L.dk * 2;
+  x.bytes[XK_CS] = (size_t)R.L.bs * sizeof(float2);
+  x.acc = R.acc();
+  x.compute = [&](int k, const void* blk, const void*) {
+    return fwd_step_main(R, static_cast<const __nv_bfloat16*>(blk), k == 0, pos, st);
+  };
+  x.merge = [&](float2* cs) { fwd_step_merge(R, cs, st); };
+  x.finish = [&](const float2* cs) { fwd_finish(R, cs, lse_a, lse_b, pos, R.acc(), st); };
+  TRY(run_ring(comm, ops, x, st));
+  launch_loss_write(R.acc(), loss, b, st);
+  TRY(comm_async_check(comm));
+  INFCL_CUDA_TRY(cudaGetLastError());
+  return INFCL_OK;
+}
+
+extern "C" infcl_status infcl_ntxent_backward(infcl_comm comm, const void* A_local, const void* B_local,
+                                              infcl_dtype dt, int64_t b, int d, float s, int rank, int world,
+                                              const float* lse_a, const float* lse_b, const float* pos,
+                                              const float* grad, float* dA, float* dB, void* ws, size_t ws_bytes,
+                                              void* stream) {
+  const size_t need = infcl_comm_workspace_bytes(world > 1 ? comm : nullptr, b, d, world, dt);
+  TRY(validate(A_local, B_local, dt, b, d, s, rank, world, ws, ws_bytes, need));
+  TRY(ntxent_check(dt, world, comm));
+  if (!lse_a || !lse_b || !pos || !grad || !dA || !dB) return fail(INFCL_ERR_INVALID_ARG, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PairCarveOut carve(ring_carveout(comm, world));
+  Rank R;
+  TRY(prepare_rank(R, A_local, B_local, dt, b, d, s, world, ws, st, world == 1 || ring_in_ws(comm)));
+  if (world > 1) TRY(ring_setup(comm, R, rank, world));
+  // own2(0) = r_A, own2(1) = r_B (log2); dA starts as the exact positive-pair term of the (A, B) block
+  TRY(bwd_begin(R, lse_a, lse_b, pos, grad, dA, st));
+  const size_t blk_bytes = (size_t)R.L.bs * R.L.dk * 2, lse_bytes = (size_t)R.L.bs * sizeof(float);
+  auto block = [&](const __nv_bfloat16* rows, const float* rows2, const __nv_bfloat16* own_blk,
+                   const float* own_cols2, bool self, float* out) -> infcl_status {
+    if (world == 1) return bwd_step(R, rows, rows2, own_blk, own_cols2, true, out, R.L.d, grad, st, self);
+    std::vector<ROp> ops;
+    bwd_ring_ops(world, rank, ops);
+    RingCtx x;
+    x.own = own_blk;
+    x.ownl = own_cols2;
+    x.bytes[XK_BLK] = blk_bytes;
+    x.bytes[XK_LSE] = lse_bytes;
+    x.compute = [&](int k, const void* blk, const void* lse) {
+      return bwd_step(R, rows, rows2, static_cast<const __nv_bfloat16*>(blk), static_cast<const float*>(lse), k == 0,
+                      out, R.L.d, grad, st, self);
+    };
+    return run_ring(comm, ops, x, st);
+  };
+  for (int pass = 0; pass < 2; ++pass) {
+    const __nv_bfloat16* rows = pass == 0 ? R.A : R.B;
+    const __nv_bfloat16* other = pass == 0 ? R.B : R.A;
+    const float* rows2 = R.own2(pass);
+    const float* other2 = R.own2(1 - pass);
+    float* out = pass == 0 ? dA : dB;
+    if (pass == 1) diag_init(R, 1, dB, pos, lse_a, lse_b, grad, st);
+    TRY(block(rows, rows2, other, other2, false, out));  // the other views: positives on the diagonal
+    TRY(block(rows, rows2, rows, rows2, true, out));     // the same side's views: self-similarity excluded
+  }
+  if (world > 1) TRY(comm_async_check(comm));
+  INFCL_CUDA_TRY(cudaGetLastError());
+  return INFCL_OK;
 }
 
 // ------------------------------------------------------------------------------------------ virtual ring

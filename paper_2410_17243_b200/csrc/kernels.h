@@ -29,6 +29,7 @@ struct PassArgs {
   int diag_on;          // B is A's own block: the positive pair of row i is column i + row_off
   int row_off;          // diagonal: the positive pair of local row i is local column i + row_off
   int slots_merge;      // forward: column slots are pre-initialised (-inf, 0); always merge into them
+  int self_mask;        // column i + row_off is row i's own view: excluded from LSEs and G (NT-Xent, N2)
   // forward outputs (per pass / ring step)
   float2* col_slots;    // [2 * npairs][slot_ld] (m2, sigma) partials (workspace)
   long long slot_ld;

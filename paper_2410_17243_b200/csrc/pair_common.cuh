@@ -26,6 +26,7 @@ struct KParams {
   long long n_items;
   float k2, scale;
   int diag_on, row_off, slots_merge;
+  int self_mask;  // column i + row_off of row i is the row's own view: excluded (-inf / G = 0), NT-Xent self-similarity
   int pair_commit;  // even ring: one tcgen05.commit per two stages (empty[even] releases the pair)
   float2* col_slots;
   long long slot_ld;
@@ -161,13 +162,16 @@ __device__ __forceinline__ float4 fwd_chunk_stats(float (&v)[64], uint32_t lchun
       }
     }
   }
-  const bool ragged = !(rok[0] && rok[1] && rok[2] && rok[3]) || cb + 64 > p.ncols;
+  // self-masked launch (NT-Xent, reading N2): the warp's 32 rows meet their own column in this chunk
+  const bool selfd = p.self_mask && rowbase + p.row_off < cb + 64 && rowbase + p.row_off + 32 > cb;
+  const bool ragged = selfd || !(rok[0] && rok[1] && rok[2] && rok[3]) || cb + 64 > p.ncols;
   if (ragged) {
 #pragma unroll
     for (int i = 0; i < 64; ++i) {
       const int ri = (i >> 5) * 2 + ((i >> 1) & 1);
       const int col = cb + 8 * ((i >> 2) & 7) + 2 * t0 + (i & 1);
-      v[i] = (rok[ri] && col < p.ncols) ? v[i] : -INFINITY;
+      const int row = rowbase + 16 * (ri >> 1) + 8 * (ri & 1);
+      v[i] = (rok[ri] && col < p.ncols && !(selfd && col == row + p.row_off)) ? v[i] : -INFINITY;
     }
   }
   float ml[4];  // per-row local maxima (log2 units)
@@ -250,7 +254,8 @@ __device__ __forceinline__ float4 fwd_chunk_stats(float (&v)[64], uint32_t lchun
     for (int i = 0; i < 64; ++i) {
       const int ri = (i >> 5) * 2 + ((i >> 1) & 1);
       const int col = cb + 8 * ((i >> 2) & 7) + 2 * t0 + (i & 1);
-      y[i] = (rok[ri] && col < p.ncols) ? y[i] * k2 : -INFINITY;
+      const int row = rowbase + 16 * (ri >> 1) + 8 * (ri & 1);
+      y[i] = (rok[ri] && col < p.ncols && !(selfd && col == row + p.row_off)) ? y[i] * k2 : -INFINITY;
     }
 #pragma unroll
     for (int rho = 0; rho < 8; ++rho)

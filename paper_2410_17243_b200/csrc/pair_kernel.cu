@@ -310,7 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int buf = BWD ? 0 : (tile_ctr & (kNB - 1));
         const int cb = ct * kColsPerTile + h * 128 + u * 64;  // global column of this thread's column 0
         const int igd = ig + p.row_off;  // the column holding this row's positive pair
-        const bool diag_tile = p.diag_on && igd >= cb && igd < cb + 64;
+        const bool diag_tile = (p.diag_on || p.self_mask) && igd >= cb && igd < cb + 64;
         const bool clean = row_ok && (cb + 64 <= p.ncols) && !diag_tile;
         // backward: G_ij = 2^{y-r2_i} + 2^{y-c2_j} = E (1 + p_i q_j) with E = 2^{y-r2_i}, p_i = 2^{r2_i-cmin},
         // q_j = 2^{cmin-c2_j} (cmin = the tile's smallest column LSE of this warp): one exponential per logit.
@@ -422,8 +422,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 64; j += 2) {
               const int jg = cb + j;
-              const bool ok0 = row_ok && jg < p.ncols && !(p.diag_on && jg == igd);
-              const bool ok1 = row_ok && jg + 1 < p.ncols && !(p.diag_on && jg + 1 == igd);
+              const bool dm = p.diag_on || p.self_mask;  // positive (added exactly later) or self (excluded)
+              const bool ok0 = row_ok && jg < p.ncols && !(dm && jg == igd);
+              const bool ok1 = row_ok && jg + 1 < p.ncols && !(dm && jg + 1 == igd);
               pk[j / 2] &= (ok0 ? 0x0000FFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
             }
           }
@@ -541,6 +542,7 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.k2 = a.scale * 1.4426950408889634f;
   k.scale = a.scale;
   k.diag_on = a.diag_on;
+  k.self_mask = a.self_mask;
   k.row_off = a.row_off;
   k.slots_merge = a.slots_merge;
   k.col_slots = a.col_slots;

@@ -280,6 +280,7 @@ infcl_status launch_wide_forward(const PassArgs& a, cudaStream_t s) {
   k.k2 = a.scale * 1.4426950408889634f;
   k.scale = a.scale;
   k.diag_on = a.diag_on;
+  k.self_mask = a.self_mask;
   k.row_off = a.row_off;
   k.slots_merge = a.slots_merge;
   k.col_slots = a.col_slots;

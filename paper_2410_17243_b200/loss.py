@@ -154,6 +154,63 @@ def infcl_backward(I_local, T_local, b: int, logit_scale: float, row_lse, col_ls
     return dI, dT
 
 
+def ntxent_forward(A_local, B_local, b: int, logit_scale: float, rank: int = 0, world: int = 1, comm=None,
+                   workspace=None):
+    """NT-Xent (SimCLR) over the 2b views [A; B] (include/infcl.h infcl_ntxent_forward): returns (loss, lse_a,
+    lse_b, pos) for this rank's examples; b = global number of examples."""
+    A_local, B_local = _check_features(A_local, B_local)
+    bs, d = A_local.shape
+    dev = A_local.device
+    la = torch.empty(bs, device=dev, dtype=torch.float32)
+    lb = torch.empty_like(la)
+    pos = torch.empty_like(la)
+    loss = torch.empty((), device=dev, dtype=torch.float32)
+    ws = workspace if workspace is not None else alloc_workspace(b, d, world, A_local.dtype, dev, comm=comm)
+    L.call("infcl_ntxent_forward", comm.handle if comm is not None else None, A_local.data_ptr(), B_local.data_ptr(),
+           _dtype_code(A_local), b, d, float(logit_scale), rank, world, la.data_ptr(), lb.data_ptr(), pos.data_ptr(),
+           loss.data_ptr(), ws.data_ptr(), ws.numel(), _stream())
+    return loss, la, lb, pos
+
+
+def ntxent_backward(A_local, B_local, b: int, logit_scale: float, lse_a, lse_b, pos, grad_loss, rank: int = 0,
+                    world: int = 1, comm=None, workspace=None):
+    """Returns (dA, dB) fp32 = g dL/dA, g dL/dB of the NT-Xent loss for this rank's examples."""
+    A_local, B_local = _check_features(A_local, B_local)
+    bs, d = A_local.shape
+    dev = A_local.device
+    dA = torch.empty(bs, d, device=dev, dtype=torch.float32)
+    dB = torch.empty_like(dA)
+    g = grad_loss.detach().to(device=dev, dtype=torch.float32).reshape(()).contiguous()
+    ws = workspace if workspace is not None else alloc_workspace(b, d, world, A_local.dtype, dev, comm=comm)
+    L.call("infcl_ntxent_backward", comm.handle if comm is not None else None, A_local.data_ptr(), B_local.data_ptr(),
+           _dtype_code(A_local), b, d, float(logit_scale), rank, world, lse_a.data_ptr(), lse_b.data_ptr(),
+           pos.data_ptr(), g.data_ptr(), dA.data_ptr(), dB.data_ptr(), ws.data_ptr(), ws.numel(), _stream())
+    return dA, dB
+
+
+class _NTXentFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, A_local, B_local, b, logit_scale, rank, world, comm):
+        loss, la, lb, pos = ntxent_forward(A_local, B_local, b, logit_scale, rank, world, comm)
+        ctx.save_for_backward(A_local, B_local, la, lb, pos)
+        ctx.meta = (b, logit_scale, rank, world, comm)
+        return loss
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        A_local, B_local, la, lb, pos = ctx.saved_tensors
+        b, s, rank, world, comm = ctx.meta
+        dA, dB = ntxent_backward(A_local, B_local, b, s, la, lb, pos, grad_out, rank, world, comm)
+        return dA.to(A_local.dtype), dB.to(B_local.dtype), None, None, None, None, None
+
+
+def ntxent_loss(A_local: torch.Tensor, B_local: torch.Tensor, logit_scale: float, comm: "RingComm | None" = None):
+    """Differentiable NT-Xent (SimCLR) loss over the global batch of view pairs (this rank's shards)."""
+    world = comm.world if comm is not None else 1
+    rank = comm.rank if comm is not None else 0
+    return _NTXentFunction.apply(A_local, B_local, A_local.shape[0] * world, float(logit_scale), rank, world, comm)
+
+
 def comm_sum(t: torch.Tensor, comm=None) -> torch.Tensor:
     """Sum a per-rank partial over the ranks of ``comm``'s ring, in place: a no-op for a local loss (comm None or
     world 1) -- never over an unrelated default process group (a DDP job computing a local loss must not add

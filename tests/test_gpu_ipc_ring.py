@@ -133,3 +133,53 @@ def test_ipc_ring_cfg3_onehot_closed_form(tmp_path):
         want[np.arange(len(rows)), rows % K_] = s32 / b * (m * p - 1.0)
         for got in (part["dI"], part["dT"]):
             assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 2e-3
+
+
+def _worker_ntxent(rank, world, port, b, d, s, outdir):
+    if ROOT not in sys.path:
+        sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2410_17243_b200 import loss as K
+        from synth import make_features, shard
+        torch.cuda.set_device(0)
+        A, B = make_features(b, d, seed=6, dist="paired")
+        Ai, Bi = shard(A, rank, world).cuda(), shard(B, rank, world).cuda()
+        comm = K.RingComm(transport="ipc", max_b=b, max_d=d)
+        g = torch.tensor(0.5, device="cuda")
+        for it in range(2):
+            loss, la, lb, pos = K.ntxent_forward(Ai, Bi, b, s, rank, world, comm)
+            dA, dB = K.ntxent_backward(Ai, Bi, b, s, la, lb, pos, g, rank, world, comm)
+            torch.cuda.synchronize()
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), loss=loss.item(), la=la.cpu().numpy(), lb=lb.cpu().numpy(),
+                 dA=dA.cpu().numpy(), dB=dB.cpu().numpy())
+        dist.barrier()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("b,d,world", [(2 * 1024, 256, 2), (3 * 520, 64, 3)])
+def test_ipc_ring_ntxent(tmp_path, b, d, world):
+    """NT-Xent as a world-process ring: the (B, B) and (A, A) self-similarity rings and the
+    (A, B) ring per forward, four backward rings; gathered results against oracle.ntxent at north-star gates."""
+    from oracle import ntxent as N
+    from synth import make_features
+    s = 14.2857
+    mp.start_processes(_worker_ntxent, args=(world, _free_port(), b, d, s, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    parts = [np.load(tmp_path / f"rank{q}.npz") for q in range(world)]
+    A, B = make_features(b, d, seed=6, dist="paired")
+    ref = N.forward(A, B, s)
+    rdA, rdB = N.backward(A, B, s, 0.5)
+    for p in parts:
+        assert float(p["loss"]) == float(parts[0]["loss"])
+    assert abs(float(parts[0]["loss"]) - ref["loss"]) <= 1e-4 * abs(ref["loss"])
+    assert np.abs(np.concatenate([p["la"] for p in parts]) - ref["r_a"]).max() <= 2e-3
+    assert np.abs(np.concatenate([p["lb"] for p in parts]) - ref["r_b"]).max() <= 2e-3
+    for key, want in (("dA", rdA), ("dB", rdB)):
+        got = np.concatenate([p[key] for p in parts])
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 2e-3
