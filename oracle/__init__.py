@@ -28,6 +28,8 @@ from .infonce import (  # noqa: F401
     streamed_forward,
     streamed_grad_scale,
     sampled_row_grads,
+    streamed_row_lse,
+    streamed_row_grads,
     ring_schedule,
     ring_forward,
     ring_backward,

@@ -260,6 +260,39 @@ def sampled_row_grads(A, B, s: float, lse_a, lse_b, rows, g: float = 1.0) -> np.
     return s32 * (G @ B)
 
 
+def streamed_row_lse(A_rows, B, s: float, chunk: int = 131072) -> np.ndarray:
+    """Exact fp64 LSE over ALL rows of B of x_ij = s <A_rows_i, B_j> for a sample of rows (A_rows [k][d]),
+    streamed over row chunks of B with the Eq.4 merge (reading Q1/Q2): O(k * chunk) memory, so usable at the
+    paper's 4M batch where B in fp64 alone is 26 GB.  B may be a bf16 torch tensor (widened chunk by chunk)."""
+    A_rows = to_f64(A_rows)
+    s32 = _scale32(s)
+    out = np.full(A_rows.shape[0], NEG_INF)
+    for j0 in range(0, B.shape[0], chunk):
+        X = s32 * (A_rows @ to_f64(B[j0:j0 + chunk]).T)
+        out = merge_lse(out, tile_lse(X))
+    return out
+
+
+def streamed_row_grads(A_rows, B, s: float, lse_rows, lse_b, rows, g: float = 1.0, chunk: int = 131072) -> np.ndarray:
+    """``sampled_row_grads`` streamed over row chunks of B: dA_i = s sum_j G_ij B_j for global rows ``rows``
+    (A_rows = A[rows]), G_ij = g/(2b)(e^{x_ij - lse_rows_i} + e^{x_ij - lse_b_j}) - (g/b)[j == rows_i]."""
+    A_rows = to_f64(A_rows)
+    s32 = _scale32(s)
+    b = B.shape[0]
+    rows = np.asarray(rows, dtype=np.int64)
+    lse_rows = np.asarray(lse_rows, dtype=np.float64)
+    lse_b = np.asarray(lse_b, dtype=np.float64)
+    out = np.zeros_like(A_rows)
+    for j0 in range(0, b, chunk):
+        Bc = to_f64(B[j0:j0 + chunk])
+        X = s32 * (A_rows @ Bc.T)
+        G = (g / (2.0 * b)) * (np.exp(X - lse_rows[:, None]) + np.exp(X - lse_b[None, j0:j0 + Bc.shape[0]]))
+        hit = (rows >= j0) & (rows < j0 + Bc.shape[0])
+        G[np.nonzero(hit)[0], rows[hit] - j0] -= g / b
+        out += s32 * (G @ Bc)
+    return out
+
+
 # --------------------------------------------------------------------------------------------------
 # Cross-GPU ring (Alg.1, Alg.3) simulated in one process on materialised shards
 # --------------------------------------------------------------------------------------------------

@@ -114,16 +114,23 @@ def shard(x: torch.Tensor, rank: int, world: int) -> torch.Tensor:
     return x[rank * bs:(rank + 1) * bs]
 
 
-def make_features_device(b: int, d: int, seed: int, device, dtype=torch.bfloat16):
-    """Fast on-device generator for benchmark-sized batches (same distribution, different stream):
-    torch's CUDA Philox, fp32 normalisation, RNE rounding. Used by bench.py only."""
+def make_features_device(b: int, d: int, seed: int, device, dtype=torch.bfloat16, dist: str = "independent",
+                         sigma: float = 1.0):
+    """Fast on-device generator for benchmark- and paper-sized batches (same distributions, different stream):
+    torch's CUDA Philox, fp32 normalisation, RNE rounding.  dist "independent" or "paired"
+    (T = normalise(I + sigma * normalise(eps)), as make_features)."""
     gen = torch.Generator(device=device)
     gen.manual_seed(seed)
-    I = torch.randn(b, d, device=device, generator=gen, dtype=torch.float32)
-    T = torch.randn(b, d, device=device, generator=gen, dtype=torch.float32)
-    I = torch.nn.functional.normalize(I, dim=1).to(dtype)
+    I = torch.nn.functional.normalize(torch.randn(b, d, device=device, generator=gen, dtype=torch.float32), dim=1)
+    if dist == "independent":
+        T = torch.randn(b, d, device=device, generator=gen, dtype=torch.float32)
+    elif dist == "paired":
+        T = torch.randn(b, d, device=device, generator=gen, dtype=torch.float32)
+        T = I + sigma * torch.nn.functional.normalize(T, dim=1)
+    else:
+        raise ValueError(f"unknown dist {dist!r}")
     T = torch.nn.functional.normalize(T, dim=1).to(dtype)
-    return I, T
+    return I.to(dtype), T
 
 
 def make_onehot_device(b: int, d: int, K: int, device, dtype=torch.bfloat16):

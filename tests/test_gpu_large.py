@@ -199,3 +199,50 @@ def test_cfg3_random_sampled_protocol(b, world):
     c_rows[cols] = c_ex
     rdT = oracle.sampled_row_grads(T, I, S, c_rows, r, cols)
     assert rel_norm(dT.cpu().numpy()[cols], rdT) <= 2e-3
+
+
+def test_cfg5_random_sampled_protocol():
+    """cfg5 -- the paper's 4M headline batch (Table 2; b = 4194304, d = 768) -- on RANDOM paired inputs at
+    s = 14.2857, at its exact per-rank shape (b_s = 524288) through the virtual 8-rank ring (Alg.1 / Alg.3,
+    P:539-558), by the large-b protocol: exact fp64 r_i at 256 stratified rows and c_j at 256
+    columns (streamed over all 4M columns), the diagonal, the loss recomputed from the GPU's r, c and the exact
+    diagonal, 256 exact gradient rows of dI and dT (oracle.streamed_row_grads), and the O(b d) identity
+    sum <dI, I> = sum <dT, T>.  Inputs are generated on the device (synth.make_features_device, paired) and
+    widened on the host chunk by chunk."""
+    from synth import make_features_device
+    b, d, world = 4194304, 768, 8
+    Id, Td = make_features_device(b, d, seed=5, device="cuda", dist="paired")
+    g = torch.tensor(1.0, device="cuda")
+    loss, r, c, dg = K.infcl_forward_virtual(Id, Td, S, world)
+    dI, dT = K.infcl_backward_virtual(Id, Td, S, world, r, c, dg, g)
+    torch.cuda.synchronize()
+    ident_i = sum((dI[j:j + 262144].double() * Id[j:j + 262144].double()).sum().item() for j in range(0, b, 262144))
+    ident_t = sum((dT[j:j + 262144].double() * Td[j:j + 262144].double()).sum().item() for j in range(0, b, 262144))
+    rows = stratified_rows(b, 256, seed=11)
+    cols = stratified_rows(b, 256, seed=12)
+    ridx = torch.from_numpy(rows).cuda()
+    cidx = torch.from_numpy(cols).cuda()
+    dI_rows, dT_cols = dI[ridx].cpu().numpy(), dT[cidx].cpu().numpy()
+    del dI, dT
+    r, c, dg = r.cpu().numpy(), c.cpu().numpy(), dg.cpu().numpy()
+    I, T = Id.cpu(), Td.cpu()
+    del Id, Td
+    assert abs(ident_i - ident_t) <= 1e-3 * max(abs(ident_i), abs(ident_t))
+    s32 = float(np.float32(S))
+    r_ex = oracle.streamed_row_lse(I[rows], T, S)
+    c_ex = oracle.streamed_row_lse(T[cols], I, S)
+    assert np.abs(r[rows] - r_ex).max() <= 2e-3
+    assert np.abs(c[cols] - c_ex).max() <= 2e-3
+    diag_ex = np.concatenate([s32 * np.einsum("ij,ij->i", oracle.to_f64(I[j0:j0 + 262144]),
+                                              oracle.to_f64(T[j0:j0 + 262144])) for j0 in range(0, b, 262144)])
+    assert np.abs(dg - diag_ex).max() <= 2e-3
+    L = 0.5 * (np.sum(r.astype(np.float64) - diag_ex) + np.sum(c.astype(np.float64) - diag_ex)) / b
+    assert abs(loss.item() - L) <= 1e-4 * abs(L)
+    c_all = c.astype(np.float64)
+    c_all[cols] = c_ex
+    r_all = r.astype(np.float64)
+    r_all[rows] = r_ex
+    want_i = oracle.streamed_row_grads(I[rows], T, S, r_ex, c_all, rows)
+    want_t = oracle.streamed_row_grads(T[cols], I, S, c_ex, r_all, cols)
+    assert rel_norm(dI_rows, want_i) <= 2e-3
+    assert rel_norm(dT_cols, want_t) <= 2e-3

@@ -243,6 +243,22 @@ def test_streamed_and_sampled_match_full():
     assert np.allclose(dIs, f["dI"][rows], atol=1e-15) and np.allclose(dTs, f["dT"][rows], atol=1e-15)
 
 
+@pytest.mark.parametrize("chunk", [1, 7, 64, 1000])
+def test_streamed_row_lse_and_grads_match_full(chunk):
+    """The large-b (cfg5) sampled helpers streamed over column chunks equal the materialised definition (whose
+    pins are above: brute force, finite differences) for any chunking."""
+    b, d = 200, 12
+    I = rand_feats(b, d, 71)
+    T = rand_feats(b, d, 72)
+    f = O.loss_and_grads(I, T, 14.2857)
+    rows = np.array([0, 3, 64, 128, 199])
+    assert np.allclose(O.streamed_row_lse(I[rows], T, 14.2857, chunk=chunk), f["r"][rows], atol=1e-12)
+    assert np.allclose(O.streamed_row_lse(T[rows], I, 14.2857, chunk=chunk), f["c"][rows], atol=1e-12)
+    dIs = O.streamed_row_grads(I[rows], T, 14.2857, f["r"][rows], f["c"], rows, chunk=chunk)
+    dTs = O.streamed_row_grads(T[rows], I, 14.2857, f["c"][rows], f["r"], rows, chunk=chunk)
+    assert np.allclose(dIs, f["dI"][rows], atol=1e-15) and np.allclose(dTs, f["dT"][rows], atol=1e-15)
+
+
 def test_ring_schedule_spec_example_and_coverage():
     # S:297: i=2, j=3 (1-based), n=4 -> k = (i+j-1) mod n = 0  == 0-based step 2
     assert O.ring_schedule(2, 4, 2) == 0
