@@ -52,8 +52,8 @@ int infcl_diag_walk(int tiles, int KB, int ns, int mode, long long* out);
 int infcl_diag_walk2(int tiles, int KB, int ns, int mode, int nclusters, long long* out);
 
 /* Copy-path probe (scripts/experiments/overlap_probe.py): device-to-device copy of `bytes` on `stream`;
- * mode 0 = cudaMemcpyAsync, mode 1 = cudaMemcpyBatchAsync with cudaMemcpyFlagPreferOverlapWithCompute (the
- * IPC ring transport's copy).  Returns the cudaError_t of the enqueue (0 = success). */
+ * mode 0 = cudaMemcpyAsync (the IPC ring transport's copy); any other mode returns cudaErrorInvalidValue.
+ * Returns the cudaError_t of the enqueue (0 = success). */
 int infcl_diag_copy(void* dst, const void* src, size_t bytes, int mode, void* stream);
 
 /* L2 reduction-throughput probe (single-pass backward feasibility): `nblocks` CTAs each add

@@ -606,17 +606,11 @@ infcl_status flag_write(cudaStream_t stream, uint8_t* region, size_t field, uint
   return INFCL_OK;
 }
 
-// device-to-device copy on the copy engines: cudaMemcpyBatchAsync with cudaMemcpyFlagPreferOverlapWithCompute
-// (a plain cudaMemcpyAsync of device memory may run as an SM copy kernel, which cannot start while the pair
-// kernels hold every SM -- scripts/experiments/overlap_probe.py measures both)
+// device-to-device copy of one travelling block (or state) into the peer's mapped region: one cudaMemcpyAsync
+// per message (peer-to-peer across GPUs runs on the copy engines; the batched-copy API is not used because it
+// raised GPU faults on this pool)
 cudaError_t ce_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
-  cudaMemcpyAttributes at = {};
-  at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  void* dsts[1] = {dst};
-  void* srcs[1] = {const_cast<void*>(src)};
-  size_t sizes[1] = {bytes}, idx[1] = {0}, fail_idx = 0;
-  return cudaMemcpyBatchAsync(dsts, srcs, sizes, 1, &at, idx, 1, &fail_idx, st);
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st);
 }
 
 // send `bytes` of `src` to slot (kind, s) of rank r-1, and (NCCL) receive rank r+1's into our slot (kind, s);

@@ -715,18 +715,11 @@ extern "C" int infcl_diag_tma_rate3(const void* X, int nrows, int d, int mode, i
 }
 
 // ------------------------------------------------------------------ copy-path probe (diagnostic)
-// The IPC ring transport's copy: mode 0 = cudaMemcpyAsync; mode 1 = cudaMemcpyBatchAsync with
-// cudaMemcpyFlagPreferOverlapWithCompute (copy engines, so the copy can run beside kernels that hold every SM).
+// The IPC ring transport's copy (cudaMemcpyAsync device to device); only mode 0 exists.
 extern "C" int infcl_diag_copy(void* dst, const void* src, size_t bytes, int mode, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (mode == 0) return (int)cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st);
-  cudaMemcpyAttributes at = {};
-  at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  void* dsts[1] = {dst};
-  void* srcs[1] = {const_cast<void*>(src)};
-  size_t sizes[1] = {bytes}, idx[1] = {0}, fail_idx = 0;
-  return (int)cudaMemcpyBatchAsync(dsts, srcs, sizes, 1, &at, idx, 1, &fail_idx, st);
+  if (mode != 0) return (int)cudaErrorInvalidValue;
+  return (int)cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st);
 }
 
 // ------------------------------------------------------------------ L2 reduction throughput (single-pass feasibility)

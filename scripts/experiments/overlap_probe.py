@@ -1,7 +1,6 @@
 """Does a ring transfer overlap the persistent pair kernel (which holds every SM)?  Times, on one GPU:
-(a) the backward pass kernel alone, (b) a 1-GB device-to-device copy alone -- plain cudaMemcpyAsync, and
-cudaMemcpyBatchAsync with cudaMemcpyFlagPreferOverlapWithCompute (the IPC transport's copy) --, (c) each
-beside the pair kernel on a second stream, (d) the same bytes moved by an SM copy kernel (torch copy_, the way
+(a) the backward pass kernel alone, (b) a 1-GB device-to-device copy alone (cudaMemcpyAsync, the IPC
+transport's copy), (c) each beside the pair kernel on a second stream, (d) the same bytes moved by an SM copy kernel (torch copy_, the way
 an NCCL kernel moves data) beside the pair kernel."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
@@ -38,17 +37,12 @@ def rt_copy():  # plain cudaMemcpyAsync
     assert K.L.diag().infcl_diag_copy(dst.data_ptr(), src.data_ptr(), src.numel(), 0, s2.cuda_stream) == 0
 
 
-def ce_copy():  # cudaMemcpyBatchAsync + cudaMemcpyFlagPreferOverlapWithCompute (the IPC transport's copy)
-    assert K.L.diag().infcl_diag_copy(dst.data_ptr(), src.data_ptr(), src.numel(), 1, s2.cuda_stream) == 0
-
-
 def sm_copy():
     with torch.cuda.stream(s2):
         dst.copy_(src)
 
 
 for _ in range(2):
-    res = {"bwd": timed(bwd), "memcpy_1GB": timed(rt_copy), "ce_batch_copy_1GB": timed(ce_copy),
-           "sm_copy_1GB": timed(sm_copy), "bwd+memcpy": timed(lambda: (bwd(), rt_copy())),
-           "bwd+ce_batch_copy": timed(lambda: (bwd(), ce_copy())), "bwd+sm_copy": timed(lambda: (bwd(), sm_copy()))}
+    res = {"bwd": timed(bwd), "memcpy_1GB": timed(rt_copy),
+           "sm_copy_1GB": timed(sm_copy), "bwd+memcpy": timed(lambda: (bwd(), rt_copy())), "bwd+sm_copy": timed(lambda: (bwd(), sm_copy()))}
 print(json.dumps(res))
