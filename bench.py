@@ -297,7 +297,7 @@ def run_ours(args):
     value = b / (ms_step / 1e3)
     lval = float(loss.item())
 
-    # roofline of the dominant kernel (the backward pair kernel: 2 launches per ring step).  Denominator
+    # roofline of the dominant kernel (the backward pair kernel: 1 fused launch or 2 passes per ring step).  Denominator
     # (B200_PROFILING.md): the BURST cuBLAS peak for a kernel in a short step, the SUSTAINED (power-capped) one
     # only once a step lasts a second or more (b >= 512K); both fractions are reported
     peaks = measured_peaks()
@@ -312,13 +312,23 @@ def run_ours(args):
     n_l, tot_ms = prof[kind]
     avg_ms = max_over_ranks(tot_ms / max(n_l, 1))
     if kind == 1:
-        flop_per_launch = 3.0 * bs * bs * d   # algorithmic bwd 6 b_s^2 d per ring step, split over dI/dT passes
-        kname = "pair_kernel<BWD> (S recompute + G + dA GEMM; one pass of the two-pass backward)"
+        # algorithmic backward per rank and step: 6 b_s^2 d per ring step (S recompute + dI + dT), world steps; the
+        # fused single-pass kernel is 1 launch per ring step, the two-pass backward 2 (dI and dT pass)
+        per_step = n_l / args.steps
+        flop_per_launch = 6.0 * bs * bs * d * world / per_step
+        if per_step <= world:
+            kname = ("pair_kernel<BWD,GC> (fused single-pass backward: producer pairs S recompute + G + dI GEMM, "
+                     "consumer pairs dT GEMM from the G ring)")
+        else:
+            kname = "pair_kernel<BWD> (S recompute + G + dA GEMM; one pass of the two-pass backward)"
     else:
         flop_per_launch = 2.0 * bs * bs * d
         kname = "pair_kernel<FWD> (S GEMM + row/col LSE + diag)"
     achieved = flop_per_launch / (avg_ms / 1e3) / 1e12
-    traffic = ncu_traffic().get(f"{'bwd' if kind == 1 else 'fwd'}_{b}_{d}_{world}")
+    tkey = f"{'bwd' if kind == 1 else 'fwd'}_{b}_{d}_{world}"
+    if kind == 1 and n_l / args.steps <= world:
+        tkey = f"bwdfused_{b}_{d}_{world}"
+    traffic = ncu_traffic().get(tkey)
     step_tf = 8.0 * b * b * d / world / (ms_step / 1e3) / 1e12
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic, "kernel": kname, "avg_launch_ms": avg_ms, "launches": n_l,

@@ -309,6 +309,7 @@ struct Layout {
   long long slot_ld = 0;
   size_t off_slots, off_rparts, off_rstate, off_cstate, off_own2, off_ring_lse, off_ring_blk, off_expA, off_expB,
       off_dscr, off_tails, off_xstate, off_acc, total;
+  GcPlan gc{};  // fused single-pass backward (world 1, bf16): its ring shares the forward's column-slot region
 };
 
 // ring_ws: the ring's receive buffers live in the workspace (NCCL transport); the IPC transport receives
@@ -328,7 +329,15 @@ Layout make_layout(int64_t b, int d, int world, infcl_dtype dt, bool ring_ws = t
     o += align_up(bytes);
     return at;
   };
-  L.off_slots = take((size_t)2 * L.g.npairs * L.slot_ld * sizeof(float2));
+  // column slots (forward) and split-tail scratch (two-pass backward) share one region with the fused
+  // backward's step counters and G ring: the three are never live in the same launch
+  const size_t slots_b = align_up((size_t)2 * L.g.npairs * L.slot_ld * sizeof(float2));
+  // backward: per-pair partials of split tail row blocks (< 2P slots of 128 rows x dk fp32; any row range of the
+  // pass has at most P - 1 tail row blocks), combined in pair order -> deterministic gradients
+  const size_t tails_b = align_up((size_t)(2 * L.g.npairs - 1) * kRowsPerPair * L.dk * sizeof(float));
+  if (world == 1 && !L.f32) L.gc = gc_plan(L.bs, L.bs, L.dk);
+  L.off_slots = take(std::max(slots_b + tails_b, L.gc.ok ? L.gc.bytes : (size_t)0));
+  L.off_tails = L.off_slots + slots_b;
   // row partials: (row blocks + 2 x pairs) x rows-per-pair slots of whichever kernel runs (narrow or wide)
   const PassGeom gw = wide_geom(L.bs, L.bs);
   L.off_rparts = take(std::max((size_t)(L.g.n_rb + 2 * L.g.npairs) * L.g.rpp,
@@ -341,9 +350,6 @@ Layout make_layout(int64_t b, int d, int world, infcl_dtype dt, bool ring_ws = t
   L.off_expA = take(L.f32 ? (size_t)L.bs * L.dk * 2 : 0);
   L.off_expB = take(L.f32 ? (size_t)L.bs * L.dk * 2 : 0);
   L.off_dscr = take(L.f32 ? (size_t)L.bs * L.dk * sizeof(float) : 0);
-  // backward: per-pair partials of split tail row blocks (< 2P slots of 128 rows x dk fp32; any row range of the
-  // pass has at most P - 1 tail row blocks), combined in pair order -> deterministic gradients
-  L.off_tails = take((size_t)(2 * L.g.npairs - 1) * kRowsPerPair * L.dk * sizeof(float));
   // NT-Xent (infcl_ntxent_*): the travelling (unused) column state of the self-similarity rings
   L.off_xstate = take((size_t)L.bs * sizeof(float2));
   L.off_acc = take(64);
@@ -478,6 +484,31 @@ infcl_status bwd_step(Rank& R, const __nv_bfloat16* rowsA, const float* lse_rows
   a.coef_base = (float)((double)R.s / (2.0 * (double)R.b));
   a.tail_scratch = R.tails();
   return launch_pair_backward(a, st);
+}
+
+// single-pass backward of the own pair (world 1, bf16): dI (rows I) and dT (columns T) from one fused launch;
+// both outputs already hold their exact diagonal terms (diag_init).  INFCL_ERR_UNSUPPORTED = not all CTA pairs
+// co-resident (the caller falls back to the two passes)
+infcl_status bwd_fused(Rank& R, float* dI, float* dT, const float* grad, cudaStream_t st) {
+  PassArgs a{};
+  a.A = R.A;
+  a.B = R.B;
+  a.nrows = a.ncols = R.L.bs;
+  a.dk = a.ld = R.L.dk;
+  a.scale = R.s;
+  a.diag_on = 1;
+  a.lse_row2 = R.own2(0);
+  a.lse_col2 = R.own2(1);
+  a.dA = dI;
+  a.ld_dA = R.L.d;
+  a.d_out = R.L.dk;
+  a.grad = grad;
+  a.coef_base = (float)((double)R.s / (2.0 * (double)R.b));
+  a.dB = dT;
+  a.ld_dB = R.L.d;
+  a.gc_ws = R.ws + R.L.off_slots;
+  a.gc_ws_bytes = R.L.gc.bytes;
+  return launch_pair_backward_fused(a, st);
 }
 
 // ---- blocked single-rank pieces (the host end-to-end entry pipelines PCIe copies against them)
@@ -982,6 +1013,17 @@ static infcl_status backward_impl(infcl_comm comm, const void* I_local, const vo
   TRY(prepare_rank(R, I_local, T_local, dt, b, d, s, world, ws, st, world == 1 || ring_in_ws(comm)));
   if (world > 1) TRY(ring_setup(comm, R, rank, world));
   TRY(bwd_begin(R, row_lse, col_lse, diag, grad, dI, st));
+  if (world == 1 && R.L.gc.ok) {
+    diag_init(R, 1, dT, diag, row_lse, col_lse, grad, st);
+    const infcl_status fs = bwd_fused(R, dI, dT, grad, st);
+    if (fs == INFCL_OK) {
+      if (dI_ready) INFCL_CUDA_TRY(cudaEventRecord(dI_ready, st));
+      INFCL_CUDA_TRY(cudaGetLastError());
+      return INFCL_OK;
+    }
+    if (fs != INFCL_ERR_UNSUPPORTED) return fs;
+    diag_init(R, 0, dI, diag, row_lse, col_lse, grad, st);  // nothing ran: the two passes start over
+  }
   const size_t blk_bytes = (size_t)R.L.bs * R.L.dk * 2, lse_bytes = (size_t)R.L.bs * sizeof(float);
   for (int pass = 0; pass < 2; ++pass) {
     // pass 0: rows I (lse r), stream (T, c) -> dI;  pass 1: rows T (lse c), stream (I, r) -> dT

@@ -44,7 +44,21 @@ struct PassArgs {
   float coef_base;        // s / (2 b)
   float* tail_scratch;    // [2 npairs - 1][128][d_out] fp32: per-pair partials of split tail row blocks (workspace),
                           // added in pair order by launch_tail_combine (deterministic); nullptr = red.add
+  // fused backward (launch_pair_backward_fused): the column side's gradient and the G ring workspace
+  float* dB;              // [ncols][ld_dB] fp32, accumulated with red.add (dB = coef * G^T A)
+  int ld_dB;
+  void* gc_ws;            // gc_plan(nrows, ncols, dk).bytes: step counters, then the G ring
+  size_t gc_ws_bytes;
 };
+
+// fused backward plan (pair_kernel.cu gc_plan): ok = the fused kernel applies (bf16 K width <= 512, >= 2 pairs)
+struct GcPlan {
+  bool ok;
+  int npairs, pp, pc, ring;
+  long long n_steps;
+  size_t ctr_bytes, bytes;
+};
+GcPlan gc_plan(int nrows, int ncols, int dk);
 
 struct PassGeom {
   int n_rb, n_ct, npairs;
@@ -59,11 +73,14 @@ bool wide_forward_enabled();
 infcl_status launch_pair_forward(const PassArgs& a, cudaStream_t s);  // wide forward unless INFCL_FWD_NARROW
 infcl_status launch_wide_forward(const PassArgs& a, cudaStream_t s);
 infcl_status launch_pair_backward(const PassArgs& a, cudaStream_t s);
+// single-pass backward: dA and dB from one launch (producer pairs: S, G, dA; consumer pairs: dB from the G ring)
+infcl_status launch_pair_backward_fused(const PassArgs& a, cudaStream_t s);
 // launch bookkeeping shared by the pair kernels (pair_kernel.cu)
 cudaEvent_t profile_begin(cudaStream_t s);
 void profile_end(int kind, cudaEvent_t e0, cudaStream_t s);
 unsigned long long* debug_buffer(cudaStream_t s);  // INFCL_DEBUG_WAITS accumulators (zeroed) or nullptr
-void debug_report(const char* name, int npairs, cudaStream_t s);
+// prod_pairs (fused backward): CTA pairs [0, prod_pairs) are producers, the rest consumers
+void debug_report(const char* name, int npairs, cudaStream_t s, int prod_pairs = -1);
 
 // auxiliary kernels (aux_kernels.cu)
 void launch_init_state(float2* st, int n, cudaStream_t s);

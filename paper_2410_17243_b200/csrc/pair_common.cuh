@@ -15,6 +15,8 @@ namespace infcl {
 
 constexpr int kThreads = 320;  // warps 0-7 epilogue, warp 8 TMA, warp 9 MMA
 constexpr int kWarpTMA = 8, kWarpMMA = 9;
+constexpr int kThreadsGC = 352;  // fused backward: + warp 10, the producers' G store warp
+constexpr int kWarpStore = 10;
 constexpr int kBox = 8192;     // A_R / G block: 64 rows x 64 bf16 (128 B, SW128)
 constexpr int kBoxB = 16384;   // streamed B box: 128 rows x 64 bf16 (128 B, SW128)
 constexpr int kMaxStages = 16;
@@ -39,6 +41,13 @@ struct KParams {
   const float* grad;
   float coef_base;
   float* tail_scratch;      // backward: per-pair partials of split tail row blocks (deterministic) or nullptr
+  // fused backward (GC): pairs [0, gc_pp) produce (S, G, dA; G tiles -> global ring), pairs [gc_pp, npairs)
+  // consume the ring (dB^T += A^T G per column tile over each wave of gc_pp row blocks)
+  int gc_pp, gc_ring, n_stages_c;
+  uint32_t* g_ready;     // [n_steps] producer CTAs that stored their half of step g's tiles
+  uint32_t* g_consumed;  // [n_steps] 1 once step g's ring slot has been read
+  float* dB;             // dB (dT) accumulated with red.add (column side)
+  int ld_dB;
   unsigned long long* dbg;  // optional per-tag wait-cycle accumulators (INFCL_DEBUG_WAITS)
   int noepi;                // diagnostic: epilogue skips its math (results invalid; INFCL_DEBUG_NOEPI)
   int notma;                // diagnostic: producer signals stages without loading (results invalid)
@@ -49,14 +58,23 @@ struct KParams {
 // HBM once and served from L2 to the other pairs).  Tail: the remaining R = n_rb - W*P row blocks x n_ct tiles
 // are split into P contiguous ranges (row-major), so the last wave stays balanced.  Segment = consecutive
 // items of one row block; row-partial slot of a segment: rb (full waves) or n_rb + p + (rb - W*P) (tail).
+// whole_tail (fused backward): tail row block W*P + p goes whole to pair p (no row block is split, so every G
+// tile of the last wave has exactly one producer and every dA row block one drain).
 struct Sched {
   int P, W, n_ct, n_rb, pair;
   long long tb, te;  // this pair's tail range (tail item indices)
-  __device__ Sched(int n_rb_, int n_ct_, int P_, int pair_) : P(P_), n_ct(n_ct_), n_rb(n_rb_), pair(pair_) {
+  __device__ Sched(int n_rb_, int n_ct_, int P_, int pair_, bool whole_tail = false)
+      : P(P_), n_ct(n_ct_), n_rb(n_rb_), pair(pair_) {
     W = n_rb / P;
-    const long long T = (long long)(n_rb - W * P) * n_ct;
-    tb = (long long)pair * T / P;
-    te = (long long)(pair + 1) * T / P;
+    const int R = n_rb - W * P;
+    const long long T = (long long)R * n_ct;
+    if (whole_tail) {
+      tb = pair < R ? (long long)pair * n_ct : T;
+      te = pair < R ? tb + n_ct : T;
+    } else {
+      tb = (long long)pair * T / P;
+      te = (long long)(pair + 1) * T / P;
+    }
   }
   __device__ long long n_local() const { return (long long)W * n_ct + (te - tb); }
   __device__ void decode(long long k, int& rb, int& ct) const {
@@ -78,6 +96,16 @@ struct Sched {
   }
   __device__ long long seg_slot(int rb) const { return rb < W * P ? rb : (long long)n_rb + pair + (rb - W * P); }
 };
+
+// spin until a global counter (written by other CTAs with release semantics) reaches v; watchdog as mbar_wait
+__device__ __forceinline__ void spin_geq(const uint32_t* ctr, uint32_t v, int tag) {
+  if (ld_acquire_gpu(ctr) >= v) return;
+  const unsigned long long t0 = clock64();
+  while (ld_acquire_gpu(ctr) < v) {
+    __nanosleep(32);
+    if (clock64() - t0 > INFCL_WATCHDOG_CYCLES) watchdog_fire(tag, v);
+  }
+}
 
 __device__ __forceinline__ float2 merge2(float2 a, float2 b) {
   const float M = fmaxf(a.x, b.x);
@@ -139,9 +167,11 @@ __device__ __forceinline__ void ring_acquire(WaitClock<DBG>& wc, uint64_t* empty
 // in-thread, then 8 lanes (3 butterfly rounds).  Updates the running (mrow, srow) of the thread's 4 rows
 // (base-2 units), writes x_ii for diagonal rows, and returns (m0, S0, m1, S1): the (max, sum) partial of
 // columns cb + 2*lane and cb + 2*lane + 1 over the warp's 32 rows.
+// SELF: the launch may be self-masked (NT-Xent); a separate instantiation, so the CLIP kernels carry none of it.
+template <bool SELF>
 __device__ __forceinline__ float4 fwd_chunk_stats(float (&v)[64], uint32_t lchunk, int rowbase, int cb,
                                                   const KParams& p, int lane, float (&mrow)[4], float (&srow)[4]) {
-  const float k2 = p.k2;
+  float k2 = p.k2;
   const int t0 = lane & 3;
   bool rok[4];
 #pragma unroll
@@ -163,16 +193,17 @@ __device__ __forceinline__ float4 fwd_chunk_stats(float (&v)[64], uint32_t lchun
     }
   }
   // self-masked launch (NT-Xent, reading N2): the warp's 32 rows meet their own column in this chunk
-  const bool selfd = p.self_mask && rowbase + p.row_off < cb + 64 && rowbase + p.row_off + 32 > cb;
+  const bool selfd = SELF && p.self_mask && rowbase + p.row_off < cb + 64 && rowbase + p.row_off + 32 > cb;
   const bool ragged = selfd || !(rok[0] && rok[1] && rok[2] && rok[3]) || cb + 64 > p.ncols;
-  if (ragged) {
+  if (ragged) {  // scale first, then mask: at s = 0 a masked -inf times k2 = 0 would be NaN
 #pragma unroll
     for (int i = 0; i < 64; ++i) {
       const int ri = (i >> 5) * 2 + ((i >> 1) & 1);
       const int col = cb + 8 * ((i >> 2) & 7) + 2 * t0 + (i & 1);
       const int row = rowbase + 16 * (ri >> 1) + 8 * (ri & 1);
-      v[i] = (rok[ri] && col < p.ncols && !(selfd && col == row + p.row_off)) ? v[i] : -INFINITY;
+      v[i] = (rok[ri] && col < p.ncols && !(selfd && col == row + p.row_off)) ? v[i] * k2 : -INFINITY;
     }
+    k2 = 1.f;
   }
   float ml[4];  // per-row local maxima (log2 units)
 #pragma unroll
@@ -255,7 +286,7 @@ __device__ __forceinline__ float4 fwd_chunk_stats(float (&v)[64], uint32_t lchun
       const int ri = (i >> 5) * 2 + ((i >> 1) & 1);
       const int col = cb + 8 * ((i >> 2) & 7) + 2 * t0 + (i & 1);
       const int row = rowbase + 16 * (ri >> 1) + 8 * (ri & 1);
-      y[i] = (rok[ri] && col < p.ncols && !(selfd && col == row + p.row_off)) ? y[i] * k2 : -INFINITY;
+      y[i] = (rok[ri] && col < p.ncols && !(selfd && col == row + p.row_off)) ? y[i] * p.k2 : -INFINITY;
     }
 #pragma unroll
     for (int rho = 0; rho < 8; ++rho)

@@ -50,9 +50,158 @@ static void prof_clear() {
   for (auto& v : prof().ev) v.clear();
 }
 
-template <bool BWD, bool DBG>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// Consumer CTA pair of the fused backward (GC): for every wave w of gc_pp row blocks and each of its column tiles
+// ct = c, c + P_c, ... (c = pair - gc_pp, P_c = npairs - gc_pp; ct's consumer is the same in every wave, so
+// each dB element receives its per-wave partials from one thread in wave order: deterministic), accumulate
+//   dB^T (d x 256 columns) += A_w^T (d x 128 rows) * G_w,t (128 rows x 256 columns)   over the wave's tiles t
+// with tcgen05.mma.cta_group::2 M=256 (128 d-rows per SM) N=256 K=16, both operands MN-major: A rows streamed by
+// TMA from the row features (tmI, boxes of 128 rows x 64 features), G tiles from the global ring (tmG, boxes of
+// 64 rows x 64 columns).  The accumulator (NDC x 256 TMEM columns) is drained once per (wave, ct) with red.add,
+// scaled by s g / 2b.  This is Alg.4's dT~ update with the G tiles handed over through memory
+// instead of a read-modify-write of dT per tile.
+template <bool DBG>
+__device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtensorMap* tmI, const KParams& p,
+                                            uint8_t* smem, uint64_t* full, uint64_t* empty, uint64_t* gfullc,
+                                            uint64_t* gemptyc, uint64_t* dafull, uint64_t* dafree, uint32_t tbase,
+                                            int warp, int lane, uint32_t cta, int pair) {
+  const int PP = p.gc_pp, PC = p.npairs - p.gc_pp, c = pair - p.gc_pp;
+  const int nW = (p.n_rb + PP - 1) / PP;
+  // units u = ct * nparts + part: part 0 = d chunks [0, 2), part 1 = [2, NDC) (d > 512: the accumulator of a
+  // whole 768-wide column tile exceeds TMEM); unit u belongs to consumer u mod PC in every wave
+  const int nparts = p.NDC > 2 ? 2 : 1, nunits = p.n_ct * nparts;
+  uint8_t* gbuf = smem;          // 2 G buffers of 32 KB: boxes (ib, jb) at (2 ib + jb) * 8 KB
+  uint8_t* sI = smem + 2 * 32768;  // n_stages_c ring stages of 32 KB (two 128-row x 64-feature boxes)
+  const int nsc = p.n_stages_c;
+  if (warp == kWarpTMA) {
+    if (lane == 0) {
+      WaitClock<DBG> wc(p.dbg, true);
+      int stage = 0, gb = 0;
+      uint32_t ph = 0, gph = 0;
+      for (int w = 0; w < nW; ++w) {
+        const int nt = min(PP, p.n_rb - w * PP);
+        for (int un = c; un < nunits; un += PC) {
+          const int ct = un / nparts, tc0 = (un % nparts) * 2, tc1 = min(p.NDC, tc0 + 2);
+          const long long g = (long long)w * p.n_ct + ct;
+          const unsigned long long t_sp = DBG ? clock64() : 0ull;
+          spin_geq(p.g_ready + g, 2u * nt, 14);
+          if (DBG) wc.acc[0] += clock64() - t_sp;
+          fence_proxy_async_global();
+          const int slot_row = (int)((g % p.gc_ring) * PP) * kRowsPerPair;
+          for (int t = 0; t < nt; ++t) {
+            wc.wait(&gemptyc[gb], ((gph >> gb) & 1u) ^ 1u, 2);
+            gph ^= 1u << gb;
+            if (cta == 0) mbar_arrive_expect_tx(&gfullc[gb], 2 * 32768);
+            uint8_t* gd = gbuf + gb * 32768;
+#pragma unroll
+            for (int ib = 0; ib < 2; ++ib)
+#pragma unroll
+              for (int jb = 0; jb < 2; ++jb)
+                tma_load_2d_pair(gd + (2 * ib + jb) * kBox, tmG, &gfullc[gb], ((int)cta * 2 + jb) * 64,
+                                 slot_row + t * kRowsPerPair + ib * 64);
+            gb ^= 1;
+            const int r0 = (w * PP + t) * kRowsPerPair;
+            for (int tc = tc0; tc < tc1; ++tc) {
+              wc.wait(&empty[stage], ph ^ 1u, 1);
+              if (cta == 0) mbar_arrive_expect_tx(&full[stage], 2 * 32768);
+              uint8_t* dst = sI + stage * 32768;
+              const int d0 = tc * 256 + (int)cta * 128;
+              tma_load_2d_pair(dst, tmI, &full[stage], d0, r0);
+              tma_load_2d_pair(dst + kBoxB, tmI, &full[stage], d0 + 64, r0);
+              if (++stage == nsc) {
+                stage = 0;
+                ph ^= 1;
+              }
+            }
+          }
+        }
+      }
+      wc.flush(5);
+    }
+  } else if (warp == kWarpMMA) {
+    if (cta == 0) {
+      WaitClock<DBG> wc(p.dbg, lane == 0);
+      const unsigned long long t_loop = DBG ? clock64() : 0ull;
+      const uint32_t idT = idesc_bf16(256, 256, 1, 1);
+      int stage = 0, gb = 0;
+      uint32_t ph = 0, gph = 0, dph = 0;
+      for (int w = 0; w < nW; ++w) {
+        const int nt = min(PP, p.n_rb - w * PP);
+        for (int un = c; un < nunits; un += PC) {
+          const int ct = un / nparts, tc0 = (un % nparts) * 2, tc1 = min(p.NDC, tc0 + 2);
+          const long long g = (long long)w * p.n_ct + ct;
+          wc.wait(dafree, dph ^ 1u, 3, true);
+          dph ^= 1;
+          tc_fence_after();
+          for (int t = 0; t < nt; ++t) {
+            wc.wait(&gfullc[gb], (gph >> gb) & 1u, 4);
+            gph ^= 1u << gb;
+            tc_fence_after();
+            // every G tile of step g is in smem now: the ring slot may be refilled
+            if (t == nt - 1 && lane == 0) red_release_gpu_add(p.g_consumed + g, 1u);
+            __syncwarp();
+            const uint32_t b_lo = (uint32_t)smem_desc_sw128(smem_u32(gbuf + gb * 32768), kBox, 1024);  // LBO = jb box stride
+            for (int tc = tc0; tc < tc1; ++tc) {
+              wc.wait(&full[stage], ph, 5);
+              tc_fence_after();
+              const uint32_t a_lo = (uint32_t)smem_desc_sw128(smem_u32(sI + stage * 32768), kBoxB, 1024);
+              umma_stage_dT_pair(tbase + (tc - tc0) * 256, a_lo, b_lo, idT, t != 0 ? 1u : 0u);
+              umma_commit_pair_mc_warp(&empty[stage], 0x3);
+              if (++stage == nsc) {
+                stage = 0;
+                ph ^= 1;
+              }
+            }
+            umma_commit_pair_mc_warp(&gemptyc[gb], 0x3);
+            gb ^= 1;
+          }
+          umma_commit_pair_mc_warp(dafull, 0x3);
+        }
+      }
+      if (DBG) wc.acc[0] += clock64() - t_loop;
+      wc.flush(6);
+    }
+  } else if (warp < 8) {
+    // drain: warp (q, u) holds d-rows tc*256 + cta*128 + 32q + lane, columns 128u .. 128u + 127 of the tile
+    const int q = warp & 3, u = warp >> 2;
+    const float coef = p.coef_base * __ldg(p.grad);
+    WaitClock<DBG> wc(p.dbg, lane == 0);
+    uint32_t daph = 0;
+    for (int w = 0; w < nW; ++w) {
+      for (int un = c; un < nunits; un += PC) {
+        const int ct = un / nparts, tc0 = (un % nparts) * 2, tc1 = min(p.NDC, tc0 + 2);
+        wc.wait(dafull, daph, 10, true);
+        daph ^= 1;
+        const unsigned long long t_dr = DBG ? clock64() : 0ull;
+        tc_fence_after();
+        for (int tc = tc0; tc < tc1; ++tc) {
+          const int d = tc * 256 + (int)cta * 128 + q * 32 + lane;
+          for (int cc = 0; cc < 4; ++cc) {
+            const int col0 = u * 128 + cc * 32;
+            float y[32];
+            tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + (tc - tc0) * 256 + col0, y);
+            tmem_ld_wait();
+            if (d < p.d_out) {
+              const int j0 = ct * kColsPerTile + col0;
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (j0 + i < p.ncols) red_add_f32(p.dB + (long long)(j0 + i) * p.ld_dB + d, coef * y[i]);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(dafree, 0);
+        if (DBG) wc.acc[6] += clock64() - t_dr;
+      }
+    }
+    wc.flush(7);
+  }
+}
+
+template <bool BWD, bool DBG, bool GC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kThreads, 1)
     pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmI,
                 const __grid_constant__ KParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];  // SW128 operands need 1024-B alignment
   uint8_t* smem = smem_raw;
@@ -66,6 +215,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // of the dA accumulator (a second one where TMEM allows, d <= 512, measured 1-3 % slower: DESIGN.md perf log)
   constexpr int kNB = BWD ? 1 : 4;
   __shared__ __align__(8) uint64_t afull, afree, sfull[kNB], sfree[kNB], gready, gfree, dafull, dafree;
+  // fused backward: producer G tile written (local warps -> store warp); consumer G buffers
+  __shared__ __align__(8) uint64_t gstore, gfullc[2], gemptyc[2];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(16) float2 xch[2][4][2][64];  // forward column partials of a group's 2 warps (x tile parity)
   __shared__ float2 rowx[4][64];                  // forward row partials of the 4 column slices
@@ -74,12 +225,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
-  const Sched S(p.n_rb, p.n_ct, p.npairs, pair);
+  // fused backward: pairs >= gc_pp are consumers of the G ring (gc_consumer below)
+  const bool consumer = GC && pair >= p.gc_pp;
+  const Sched S(p.n_rb, p.n_ct, GC ? p.gc_pp : p.npairs, pair, GC);
   const long long nk = S.n_local();
   constexpr uint32_t kTmemCols = 512;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.n_stages; ++s) {
+    // (GC: the consumer CTAs use n_stages_c ring stages of the same arrays)
+    for (int s = 0; s < (GC ? max(p.n_stages, p.n_stages_c) : p.n_stages); ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -90,14 +244,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&sfree[b], 16);  // one arrival per epilogue warp of both CTAs
     }
     mbar_init(&gready, 16);
-    mbar_init(&gfree, 1);
+    mbar_init(&gfree, GC ? 2 : 1);  // GC: the dA MMAs' commit + the store warp's read completion
     mbar_init(&dafull, 1);
     mbar_init(&dafree, 16);
+    if (GC) {
+      mbar_init(&gstore, 8);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&gfullc[b], 1);
+        mbar_init(&gemptyc[b], 1);
+      }
+    }
     fence_mbar_init();
   }
   if (warp == kWarpTMA && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (GC) {
+      tma_prefetch_desc(&tmG);
+      tma_prefetch_desc(&tmI);
+    }
   }
   if (warp == kWarpMMA) tmem_alloc<2>(&tmem_base, kTmemCols);
   tc_fence_before();
@@ -106,7 +271,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tbase = tmem_base;
 
   const unsigned long long t_start = DBG ? clock64() : 0ull;
-  if (warp == kWarpTMA) {
+  if (GC && consumer) {
+    gc_consumer<DBG>(&tmG, &tmI, p, smem, full, empty, gfullc, gemptyc, &dafull, &dafree, tbase, warp, lane, cta,
+                pair);
+  } else if (GC && warp == kWarpStore) {
+    // ===================================================================== G store (fused backward, both CTAs)
+    // each finished G tile (this SM's 64 rows x 256 columns, 4 SW128 boxes) goes to ring slot g % gc_ring of step
+    // g = wave * n_ct + ct once the slot's previous step has been read; gfree is released when the store has read
+    // smem, ready[g] once the global writes are complete (one step behind, so stores overlap)
+    if (lane == 0) {
+      WaitClock<DBG> wc(p.dbg, true);
+      uint32_t stph = 0;
+      long long pend = -1;
+      for (long long it = 0; it < nk; ++it) {
+        int rb, ct;
+        S.decode(it, rb, ct);
+        const int w = rb / p.gc_pp;
+        const long long g = (long long)w * p.n_ct + ct;
+        wc.wait(&gstore, stph, 1);
+        stph ^= 1;
+        const unsigned long long t_sp = DBG ? clock64() : 0ull;
+        if (g >= p.gc_ring) spin_geq(p.g_consumed + (g - p.gc_ring), p.NDC > 2 ? 2u : 1u, 13);
+        if (DBG) wc.acc[2] += clock64() - t_sp;
+        fence_proxy_async_global();
+        const int row = (int)(((g % p.gc_ring) * p.gc_pp + (rb - w * p.gc_pp)) * kRowsPerPair) + (int)cta * 64;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) tma_store_2d(&tmG, sG + k * kBox, k * 64, row);
+        bulk_commit();
+        const unsigned long long t_rd = DBG ? clock64() : 0ull;
+        bulk_wait_read<0>();
+        if (DBG) wc.acc[3] += clock64() - t_rd;
+        mbar_arrive(&gfree);
+        if (pend >= 0) {
+          bulk_wait<1>();
+          fence_proxy_async_global();
+          red_release_gpu_add(p.g_ready + pend, 1u);
+        }
+        pend = g;
+      }
+      if (pend >= 0) {
+        bulk_wait<0>();
+        fence_proxy_async_global();
+        red_release_gpu_add(p.g_ready + pend, 1u);
+      }
+      wc.flush(8);
+    }
+  } else if (warp == kWarpTMA) {
     // ===================================================================== TMA producer (both CTAs)
     if (lane == 0) {
       WaitClock<DBG> wc(p.dbg, lane == 0);
@@ -363,7 +573,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             gfph ^= 1;
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(&gready, 0);
+            if (lane == 0) {
+              mbar_arrive_cluster(&gready, 0);
+              if (GC) mbar_arrive(&gstore);
+            }
           }
         } else if constexpr (!BWD) {
           // ---------------------------------------------------------- forward statistics
@@ -372,7 +585,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           // Row references are thread-local maxima (any upper bound works for shared exponentials), so rows
           // need no shuffles; column sums reduce 4 rows in-thread, then 8 lanes (3 butterfly rounds).
           const int rowbase = rb * kRowsPerPair + (int)cta * 64 + rh * 32 + (lane >> 2);
-          const float4 cs = fwd_chunk_stats(v, laddr + buf * 128, rowbase, cb, p, lane, mrow, srow);
+          const float4 cs = fwd_chunk_stats<true>(v, laddr + buf * 128, rowbase, cb, p, lane, mrow, srow);
           const float m0 = cs.x, S0 = cs.y, m1 = cs.z, S1 = cs.w;
           // release this S buffer (per warp) only after the (rare) exact fallback has re-read it
           tc_fence_before();
@@ -437,7 +650,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                          pk[c16 * 4 + 3]);
           fence_proxy_async_smem();
           __syncwarp();  // all G writes of this warp done (and cval reads before the next tile's rewrite)
-          if (lane == 0) mbar_arrive_cluster(&gready, 0);
+          if (lane == 0) {
+            mbar_arrive_cluster(&gready, 0);
+            if (GC) mbar_arrive(&gstore);  // the store warp copies the tile to the G ring
+          }
         }
         ++tile_ctr;
       }
@@ -519,7 +735,54 @@ PassGeom pass_geom(int nrows, int ncols) {
   return g;
 }
 
-template <bool BWD>
+// Fused backward plan (GC): the split of the npairs CTA pairs into gc_pp producers and npairs - gc_pp consumers
+// balances ceil(n_rb / pp) waves x n_ct producer tiles (each S + G + dA, ~ratio x a consumer tile's time) against
+// each consumer's ceil(n_ct / pc) column tiles x n_rb consumer tiles; ring = steps resident in the G ring (a
+// consumer holds its step's slot while it streams the step's pp tiles, so ~pc steps are live at a time).
+GcPlan gc_plan(int nrows, int ncols, int dk) {
+  GcPlan q{};
+  static const bool off = [] {
+    const char* e = getenv("INFCL_FUSED_BWD");
+    return e && atoi(e) == 0;
+  }();
+  const PassGeom g = pass_geom(nrows, ncols);
+  if (off || dk > kMaxD || g.npairs < 2) return q;
+  const int nparts = dk > 512 ? 2 : 1;  // consumer units per column tile (weights 2 : 1 when split)
+  double ratio = 2.5;
+  if (const char* e = getenv("INFCL_GC_RATIO")) ratio = std::max(0.1, atof(e));
+  int best_pc = 1;
+  double best = 1e300;
+  const int NDC = (dk + 255) / 256;
+  for (int pc = 1; pc < g.npairs; ++pc) {
+    // two parts per column tile: an odd consumer count gives every consumer the same mix of both parts
+    if (nparts == 2 && pc % 2 == 0) continue;
+    const int pp = g.npairs - pc;
+    // producer tile ~ ratio consumer tiles of NDC d chunks; a consumer's units cover ~NDC / pc of every column tile
+    const double prod = (double)((g.n_rb + pp - 1) / pp) * g.n_ct * ratio * NDC;
+    const double cons = (double)((g.n_ct * nparts + pc - 1) / pc) * g.n_rb * ((double)NDC / nparts);
+    const double cost = std::max(prod, cons);
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_pc = pc;
+    }
+  }
+  if (const char* e = getenv("INFCL_GC_CONSUMERS")) best_pc = std::max(1, std::min(g.npairs - 1, atoi(e)));
+  if (best >= 1e300 && !getenv("INFCL_GC_CONSUMERS")) return q;  // no admissible split (2 pairs, 2 parts)
+  q.npairs = g.npairs;
+  q.pc = best_pc;
+  q.pp = g.npairs - best_pc;
+  q.n_steps = (long long)((g.n_rb + q.pp - 1) / q.pp) * g.n_ct;
+  long long ring = q.pc + 12;
+  // >= 2: a store warp signals step g - 1 only after storing step g, which waits for step g - ring to be read
+  if (const char* e = getenv("INFCL_GC_RING")) ring = std::max(2, atoi(e));
+  q.ring = (int)std::min<long long>(ring, q.n_steps);
+  q.ctr_bytes = ((size_t)2 * q.n_steps * sizeof(uint32_t) + 1023) / 1024 * 1024;
+  q.bytes = q.ctr_bytes + (size_t)q.ring * q.pp * kRowsPerPair * kColsPerTile * 2;
+  q.ok = true;
+  return q;
+}
+
+template <bool BWD, bool GC>
 static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   if (a.dk > kMaxD) return fail(INFCL_ERR_SHAPE, "feature dim above kernel limit 768");
   const PassGeom g = pass_geom(a.nrows, a.ncols);
@@ -556,8 +819,21 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.d_out = a.d_out;
   k.grad = a.grad;
   k.coef_base = a.coef_base;
-  // deterministic tail: only where the last wave splits row blocks between pairs
-  k.tail_scratch = (BWD && a.tail_scratch && g.n_rb % g.npairs != 0) ? a.tail_scratch : nullptr;
+  // deterministic tail: only where the last wave splits row blocks between pairs (never in the fused kernel,
+  // whose tail row blocks are whole)
+  k.tail_scratch = (BWD && !GC && a.tail_scratch && g.n_rb % g.npairs != 0) ? a.tail_scratch : nullptr;
+  GcPlan q{};
+  if (GC) {
+    q = gc_plan(a.nrows, a.ncols, a.dk);
+    if (!q.ok || q.npairs != g.npairs || !a.gc_ws || a.gc_ws_bytes < q.bytes || !a.dB)
+      return fail(INFCL_ERR_INVALID_ARG, "fused backward: no plan or workspace");
+    k.gc_pp = q.pp;
+    k.gc_ring = q.ring;
+    k.g_ready = reinterpret_cast<uint32_t*>(a.gc_ws);
+    k.g_consumed = k.g_ready + q.n_steps;
+    k.dB = a.dB;
+    k.ld_dB = a.ld_dB;
+  }
   unsigned long long* dbg_buf = debug_buffer(s);
   const bool dbg_on = dbg_buf != nullptr;
   k.dbg = dbg_buf;
@@ -565,7 +841,7 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   static int static_smem = -1;
   if (static_smem < 0) {
     cudaFuncAttributes fa;
-    INFCL_CUDA_TRY(cudaFuncGetAttributes(&fa, pair_kernel<BWD, false>));
+    INFCL_CUDA_TRY(cudaFuncGetAttributes(&fa, pair_kernel<BWD, false, GC>));
     static_smem = (int)fa.sharedSizeBytes;
   }
   const long long budget = 232448 - ((static_smem + 1023) / 1024) * 1024;
@@ -577,29 +853,65 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.n_stages = ns;
   k.pair_commit = (ns % 2 == 0 && !getenv("INFCL_NO_PAIR_COMMIT")) ? 1 : 0;
   const size_t smem = fixed + (size_t)ns * k.stage_bytes;
+  if (GC) {  // consumers: 2 G buffers + I stages in the same dynamic smem
+    k.n_stages_c = std::min((int)((smem - 2 * 32768) / 32768), kMaxStages);
+    if (k.n_stages_c < 2) return fail(INFCL_ERR_SHAPE, "fused backward: smem too small for the consumer ring");
+  }
 
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmG, tmI;
   infcl_status st = make_tmap_bf16(&tmA, a.A, a.nrows, a.dk, a.ld, 64, 64);
   if (st) return st;
   if ((st = make_tmap_bf16(&tmB, a.B, a.ncols, a.dk, a.ld, 64, 128))) return st;
+  if (GC) {
+    if ((st = make_tmap_bf16(&tmG, static_cast<uint8_t*>(a.gc_ws) + q.ctr_bytes,
+                             (uint64_t)q.ring * q.pp * kRowsPerPair, kColsPerTile, kColsPerTile, 64, 64)))
+      return st;
+    if ((st = make_tmap_bf16(&tmI, a.A, a.nrows, a.dk, a.ld, 64, 128))) return st;
+  } else {
+    tmG = tmA;
+    tmI = tmA;
+  }
 
-  k.noepi = getenv("INFCL_DEBUG_NOEPI") != nullptr;
-  k.notma = getenv("INFCL_DEBUG_NOTMA") != nullptr;
-  auto kern = dbg_on ? pair_kernel<BWD, true> : pair_kernel<BWD, false>;
+  k.noepi = !GC && getenv("INFCL_DEBUG_NOEPI") != nullptr;
+  k.notma = !GC && getenv("INFCL_DEBUG_NOTMA") != nullptr;
+  auto kern = dbg_on ? pair_kernel<BWD, true, GC> : pair_kernel<BWD, false, GC>;
   INFCL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int nthreads = GC ? kThreadsGC : kThreads;
+  if (GC) {
+    // producers and consumers wait on each other: every CTA pair must be resident at once
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(2 * g.npairs);
+      cfg.blockDim = dim3(nthreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      INFCL_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, (void*)kern, &cfg));
+    }
+    if (max_clusters < g.npairs)
+      return fail(INFCL_ERR_UNSUPPORTED, "fused backward: only " + std::to_string(max_clusters) +
+                                             " CTA pairs co-resident, need " + std::to_string(g.npairs));
+    INFCL_CUDA_TRY(cudaMemsetAsync(a.gc_ws, 0, (size_t)2 * q.n_steps * sizeof(uint32_t), s));
+  }
   cudaEvent_t e0 = profile_begin(s);
-  kern<<<dim3(2 * g.npairs), dim3(kThreads), smem, s>>>(tmA, tmB, k);
+  kern<<<dim3(2 * g.npairs), dim3(nthreads), smem, s>>>(tmA, tmB, tmG, tmI, k);
   INFCL_CUDA_TRY(cudaGetLastError());
   profile_end(BWD ? 1 : 0, e0, s);
   if (k.tail_scratch) launch_tail_combine(k.tail_scratch, a.dA, a.ld_dA, a.nrows, a.d_out, g, s);
-  if (dbg_on) debug_report(BWD ? "BWD" : "FWD", g.npairs, s);
+  if (dbg_on) debug_report(GC ? "BWD(fused)" : BWD ? "BWD" : "FWD", g.npairs, s, GC ? q.pp : g.npairs);
   ++launch_counter();
   return INFCL_OK;
 }
 
 infcl_status launch_pair_forward(const PassArgs& a, cudaStream_t s) {
   if (wide_forward_enabled()) return launch_wide_forward(a, s);
-  return launch_pair<false>(a, s);
+  return launch_pair<false, false>(a, s);
 }
 
 PassGeom fwd_geom(int nrows, int ncols) { return wide_forward_enabled() ? wide_geom(nrows, ncols) : pass_geom(nrows, ncols); }
@@ -626,18 +938,19 @@ static unsigned long long*& dbg_ptr() {
 unsigned long long* debug_buffer(cudaStream_t s) {
   static const bool on = getenv("INFCL_DEBUG_WAITS") != nullptr;
   if (!on) return nullptr;
-  if (!dbg_ptr()) cudaMalloc(&dbg_ptr(), 5 * 16 * sizeof(unsigned long long));
-  cudaMemsetAsync(dbg_ptr(), 0, 5 * 16 * sizeof(unsigned long long), s);
+  if (!dbg_ptr()) cudaMalloc(&dbg_ptr(), 10 * 16 * sizeof(unsigned long long));
+  cudaMemsetAsync(dbg_ptr(), 0, 10 * 16 * sizeof(unsigned long long), s);
   return dbg_ptr();
 }
 // debug only: per-role mean wait cycles per CTA (roles: 0 TMA, 1 MMA, 2/3 epilogue lanes)
-void debug_report(const char* name, int npairs, cudaStream_t s) {
+void debug_report(const char* name, int npairs, cudaStream_t s, int prod_pairs) {
   unsigned long long* buf = dbg_ptr();
-  unsigned long long h[80];
+  unsigned long long h[160];
   cudaMemcpyAsync(h, buf, sizeof(h), cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
-  const double nctas = 2.0 * npairs;
-  fprintf(stderr, "[infcl dbg] %s kernel: mean cycles/CTA total=%.0f\n", name, h[4 * 16 + 15] / nctas);
+  if (prod_pairs < 0) prod_pairs = npairs;
+  const double nctas = 2.0 * prod_pairs, ncons = 2.0 * (npairs - prod_pairs);
+  fprintf(stderr, "[infcl dbg] %s kernel: mean cycles/CTA total=%.0f\n", name, h[4 * 16 + 15] / (2.0 * npairs));
   const char* names[12] = {"LOOP", "empty", "afree", "dafree", "gready", "full", "afull", "sfree", "sfull", "gfree",
                            "dafull/sfull-commit", "S-issue"};
   for (int role = 0; role < 4; ++role)
@@ -645,6 +958,19 @@ void debug_report(const char* name, int npairs, cudaStream_t s) {
       if (h[role * 16 + t])
         fprintf(stderr, "[infcl dbg]   role %d wait %-7s %12.0f\n", role, names[t],
                 h[role * 16 + t] / (role >= 2 ? nctas * 4 : (role == 1 ? nctas / 2 : nctas)));
+  if (prod_pairs == npairs) return;
+  // fused backward: consumer TMA (5), consumer MMA (6), consumer drain warps (7), producer G store warp (8)
+  const char* cn[4][12] = {
+      {"ready-spin", "empty", "gempty", "", "", "", "", "", "", "", "", ""},
+      {"LOOP", "", "", "dafree", "gfull", "full", "", "", "", "", "", ""},
+      {"", "", "", "", "", "", "drain", "", "", "", "dafull", ""},
+      {"", "gstore", "consumed-spin", "read-wait", "", "", "", "", "", "", "", ""}};
+  const double norm[4] = {ncons, ncons / 2, ncons * 8, nctas};
+  for (int role = 5; role < 9; ++role)
+    for (int t = 0; t < 12; ++t)
+      if (h[role * 16 + t])
+        fprintf(stderr, "[infcl dbg]   %s %-13s %12.0f\n", role == 8 ? "store   " : role == 5 ? "c-TMA   " :
+                role == 6 ? "c-MMA   " : "c-drain ", cn[role - 5][t], h[role * 16 + t] / norm[role - 5]);
 }
 
 void profile_enable(bool on) {
@@ -665,6 +991,7 @@ infcl_status profile_read(int kind, int* launches, double* total_ms) {
   *total_ms = t;
   return INFCL_OK;
 }
-infcl_status launch_pair_backward(const PassArgs& a, cudaStream_t s) { return launch_pair<true>(a, s); }
+infcl_status launch_pair_backward(const PassArgs& a, cudaStream_t s) { return launch_pair<true, false>(a, s); }
+infcl_status launch_pair_backward_fused(const PassArgs& a, cudaStream_t s) { return launch_pair<true, true>(a, s); }
 
 }  // namespace infcl

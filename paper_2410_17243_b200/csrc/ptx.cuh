@@ -160,6 +160,36 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       : "memory");
 }
 
+// 2D tile store smem -> global (bulk async-group completion), used by the fused backward's G ring
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most N of this thread's most recent bulk groups still reading their smem source / still writing
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+// order generic-proxy global accesses against async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // ------------------------------------------------------------------ tcgen05: TMEM allocation
 template <int NCTA>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
@@ -290,6 +320,30 @@ __device__ __forceinline__ void umma_stage_dA_pair(uint32_t d_tmem, uint32_t a_l
       INFCL_STEP("896", "%8") INFCL_MMA2("t")
       "}" ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate),
       "n"(BOX2), "n"(BOX2 + 2), "n"(BOX2 + 4), "n"(BOX2 + 6)
+      : "memory");
+#undef INFCL_STEP
+#undef INFCL_MMA2
+}
+// One G tile x one 256-d chunk of the fused backward's dT GEMM (dT^T += I^T G, K = the tile's 128 rows i) in
+// a single asm block: 8 MMAs of K = 16 rows.  A (I^T, MN-major, d contiguous) advances 16 rows = 2048 B
+// (128 in the >>4 field) per MMA; B (G, MN-major, j contiguous) lives in two 16-KB row halves (i 0-63, 64-127)
+// of two 64-column boxes each, so it advances 2048 B per MMA within a half and jumps +16 KB (1024) after 4.
+__device__ __forceinline__ void umma_stage_dT_pair(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
+                                                   uint32_t accumulate) {
+#define INFCL_MMA2(P) "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, " P ";\n\t"
+#define INFCL_STEP(DA, DB) "add.u32 al, %1, " DA ";\n\tadd.u32 bl, %2, " DB ";\n\tmov.b64 a, {al, hi};\n\tmov.b64 b, {bl, hi};\n\t"
+  asm volatile(
+      "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a, b;\n\t.reg .b32 al, bl, hi;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\tmov.b32 hi, 0x40004040;\n\t"
+      INFCL_STEP("0", "0") INFCL_MMA2("p")
+      INFCL_STEP("128", "128") INFCL_MMA2("t")
+      INFCL_STEP("256", "256") INFCL_MMA2("t")
+      INFCL_STEP("384", "384") INFCL_MMA2("t")
+      INFCL_STEP("512", "1024") INFCL_MMA2("t")
+      INFCL_STEP("640", "1152") INFCL_MMA2("t")
+      INFCL_STEP("768", "1280") INFCL_MMA2("t")
+      INFCL_STEP("896", "1408") INFCL_MMA2("t")
+      "}" ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate)
       : "memory");
 #undef INFCL_STEP
 #undef INFCL_MMA2

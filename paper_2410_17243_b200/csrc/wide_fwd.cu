@@ -35,7 +35,7 @@ constexpr int kWRows = 256;       // stationary rows per CTA pair (128 per SM)
 constexpr int kWStage = 32768;    // ring stage per SM: A block 16 KB + B block 16 KB (one 64-wide K step)
 constexpr int kWBufCols = 256;    // TMEM columns per S buffer
 
-template <bool DBG, bool RESA>
+template <bool DBG, bool RESA, bool SELF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     wide_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ KParams p) {
@@ -191,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (DBG && p.noepi) {
             cs = make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
           } else {
-            cs = fwd_chunk_stats(v, lchunk, rowbase, cb, p, lane, mrow, srow);
+            cs = fwd_chunk_stats<SELF>(v, lchunk, rowbase, cb, p, lane, mrow, srow);
           }
           if (ch == 1) {  // release this S buffer (per warp) after the last TMEM read of the tile
             tc_fence_before();
@@ -292,7 +292,7 @@ infcl_status launch_wide_forward(const PassArgs& a, cudaStream_t s) {
   static int static_smem = -1;
   if (static_smem < 0) {
     cudaFuncAttributes fa;
-    INFCL_CUDA_TRY(cudaFuncGetAttributes(&fa, wide_fwd_kernel<false, false>));
+    INFCL_CUDA_TRY(cudaFuncGetAttributes(&fa, wide_fwd_kernel<false, false, false>));
     static_smem = (int)fa.sharedSizeBytes;
   }
   const long long budget = 232448 - ((static_smem + 1023) / 1024) * 1024;
@@ -314,8 +314,11 @@ infcl_status launch_wide_forward(const PassArgs& a, cudaStream_t s) {
   if ((st = make_tmap_bf16(&tmB, a.B, a.ncols, a.dk, a.ld, 64, 128))) return st;
   k.noepi = getenv("INFCL_DEBUG_NOEPI") != nullptr;
   k.notma = getenv("INFCL_DEBUG_NOTMA") != nullptr;
-  auto kern = resa ? (dbg ? wide_fwd_kernel<true, true> : wide_fwd_kernel<false, true>)
-                  : (dbg ? wide_fwd_kernel<true, false> : wide_fwd_kernel<false, false>);
+  // self-masked (NT-Xent) launches use their own instantiation: the self mask in the CLIP kernel's epilogue cost
+  // register spills and 17 % forward time (round-2 bench)
+  auto kern = a.self_mask ? (resa ? wide_fwd_kernel<false, true, true> : wide_fwd_kernel<false, false, true>)
+              : resa ? (dbg ? wide_fwd_kernel<true, true, false> : wide_fwd_kernel<false, true, false>)
+                     : (dbg ? wide_fwd_kernel<true, false, false> : wide_fwd_kernel<false, false, false>);
   INFCL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0 = profile_begin(s);
   kern<<<dim3(2 * g.npairs), dim3(kThreads), smem, s>>>(tmA, tmB, k);

@@ -54,21 +54,3 @@ def test_pair_m128_2x2_layout():
         if not close(out[c], exp):
             # diagnostic: find for each lane which (row, col-offset) it matches
             pytest.fail(f"cta {c}: layout mismatch; out[:, :4]={out[c, ::16, :4]} ref rows={ref[::16, :4]}")
-
-
-@pytest.mark.parametrize("fmt", [2, 3])
-def test_pair_m256_f16_operands(fmt):
-    """tcgen05.mma.kind::f16 with B (fmt 2) or both operands (fmt 3) in fp16 (descriptor format fields),
-    the dA GEMM's shape (M=256 pair, MN-major A): D against an fp32 matmul of the same fp16 / bf16 values."""
-    g = torch.Generator().manual_seed(40 + fmt)
-    A = torch.randn(256, 128, generator=g)
-    B = torch.randn(128, 128, generator=g)
-    A16 = A.to(torch.float16) if fmt & 1 else A.to(torch.bfloat16)
-    B16 = B.to(torch.float16)
-    out = torch.full((2, 128, 128), float("nan"), device="cuda")
-    L.diag_call("infcl_probe_umma", A16.t().contiguous().cuda().data_ptr(), B16.cuda().data_ptr(), 256, 128, 128, 1,
-                2, fmt, out.data_ptr(), 128, torch.cuda.current_stream().cuda_stream)
-    torch.cuda.synchronize()
-    ref = A16.float() @ B16.float().t()
-    out = out.cpu()
-    assert close(out[0], ref[:128]) and close(out[1], ref[128:]), (out[0, :2, :8], ref[:2, :8])
