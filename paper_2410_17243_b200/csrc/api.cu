@@ -1203,15 +1203,25 @@ extern "C" infcl_status infcl_ntxent_backward(infcl_comm comm, const void* A_loc
     };
     return run_ring(comm, ops, x, st);
   };
+  // world 1, bf16: the (A, B) block's two passes as one fused single-pass launch (dA rows and dB columns)
+  bool pair_done = false;
+  if (world == 1 && R.L.gc.ok) {
+    diag_init(R, 1, dB, pos, lse_a, lse_b, grad, st);
+    const infcl_status fs = bwd_fused(R, dA, dB, grad, st);
+    if (fs != INFCL_OK && fs != INFCL_ERR_UNSUPPORTED) return fs;
+    pair_done = fs == INFCL_OK;
+  }
   for (int pass = 0; pass < 2; ++pass) {
     const __nv_bfloat16* rows = pass == 0 ? R.A : R.B;
     const __nv_bfloat16* other = pass == 0 ? R.B : R.A;
     const float* rows2 = R.own2(pass);
     const float* other2 = R.own2(1 - pass);
     float* out = pass == 0 ? dA : dB;
-    if (pass == 1) diag_init(R, 1, dB, pos, lse_a, lse_b, grad, st);
-    TRY(block(rows, rows2, other, other2, false, out));  // the other views: positives on the diagonal
-    TRY(block(rows, rows2, rows, rows2, true, out));     // the same side's views: self-similarity excluded
+    if (!pair_done) {
+      if (pass == 1) diag_init(R, 1, dB, pos, lse_a, lse_b, grad, st);
+      TRY(block(rows, rows2, other, other2, false, out));  // the other views: positives on the diagonal
+    }
+    TRY(block(rows, rows2, rows, rows2, true, out));  // the same side's views: self-similarity excluded
   }
   if (world > 1) TRY(comm_async_check(comm));
   INFCL_CUDA_TRY(cudaGetLastError());

@@ -15,8 +15,8 @@ namespace infcl {
 
 constexpr int kThreads = 320;  // warps 0-7 epilogue, warp 8 TMA, warp 9 MMA
 constexpr int kWarpTMA = 8, kWarpMMA = 9;
-constexpr int kThreadsGC = 352;  // fused backward: + warp 10, the producers' G store warp
-constexpr int kWarpStore = 10;
+constexpr int kThreadsGC = 352;  // fused backward: + warp 10, the producers' G ring signal warp
+constexpr int kWarpSignal = 10;
 constexpr int kBox = 8192;     // A_R / G block: 64 rows x 64 bf16 (128 B, SW128)
 constexpr int kBoxB = 16384;   // streamed B box: 128 rows x 64 bf16 (128 B, SW128)
 constexpr int kMaxStages = 16;
@@ -44,7 +44,10 @@ struct KParams {
   // fused backward (GC): pairs [0, gc_pp) produce (S, G, dA; G tiles -> global ring), pairs [gc_pp, npairs)
   // consume the ring (dB^T += A^T G per column tile over each wave of gc_pp row blocks)
   int gc_pp, gc_ring, n_stages_c;
-  uint32_t* g_ready;     // [n_steps] producer CTAs that stored their half of step g's tiles
+  int gc_hint;  // L2 policies (INFCL_GC_HINT bits): 1 consumer G loads evict_first, 2 producer G stores evict_last,
+                // 4 consumer A loads evict_last
+  uint16_t* g_ring;      // [gc_ring * gc_pp * 128][256] bf16 G tiles (row-major; TMA view: tmG)
+  uint32_t* g_ready;     // [n_steps] producer CTAs (2 per pair) whose rows of step g's tiles are in the ring
   uint32_t* g_consumed;  // [n_steps] 1 once step g's ring slot has been read
   float* dB;             // dB (dT) accumulated with red.add (column side)
   int ld_dB;

@@ -50,33 +50,46 @@ static void prof_clear() {
   for (auto& v : prof().ev) v.clear();
 }
 
-// Consumer CTA pair of the fused backward (GC): for every wave w of gc_pp row blocks and each of its column tiles
-// ct = c, c + P_c, ... (c = pair - gc_pp, P_c = npairs - gc_pp; ct's consumer is the same in every wave, so
-// each dB element receives its per-wave partials from one thread in wave order: deterministic), accumulate
-//   dB^T (d x 256 columns) += A_w^T (d x 128 rows) * G_w,t (128 rows x 256 columns)   over the wave's tiles t
-// with tcgen05.mma.cta_group::2 M=256 (128 d-rows per SM) N=256 K=16, both operands MN-major: A rows streamed by
-// TMA from the row features (tmI, boxes of 128 rows x 64 features), G tiles from the global ring (tmG, boxes of
-// 64 rows x 64 columns).  The accumulator (NDC x 256 TMEM columns) is drained once per (wave, ct) with red.add,
-// scaled by s g / 2b.  This is Alg.4's dT~ update with the G tiles handed over through memory
-// instead of a read-modify-write of dT per tile.
+// Consumer CTA pair of the fused backward (GC): for every wave w of gc_pp row blocks and each of its units (column
+// tile ct, d-chunk part) u = c, c + P_c, ... (c = pair - gc_pp, P_c = npairs - gc_pp; a unit's consumer is the same in
+// every wave, so each dB element receives its per-wave partials from one thread in wave order: deterministic),
+// accumulate
+//   dB (256 columns j x 256-d chunks) += G_w,t^T (j x 128 rows i) * A_w,t (128 rows i x d)   over the wave's tiles t
+// with tcgen05.mma.cta_group::2 M=256 (128 columns j per SM) N=256 K=16, both operands MN-major: G tiles from the
+// global ring (tmG, boxes of 64 rows x 64 columns), A rows (tmI, boxes of 128 rows x 64 features), one ring of 32-KB
+// stages (per tile: one G stage, then one stage per d chunk).  TMEM lane = column j, TMEM column = feature d, so the
+// drain (once per unit and wave, scaled by s g / 2b) adds 4 consecutive features per red.global.add.v4.f32.  This is
+// Alg.4's dT~ update with the G tiles handed over through memory instead of a read-modify-write of dT
+// per tile.
 template <bool DBG>
 __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtensorMap* tmI, const KParams& p,
-                                            uint8_t* smem, uint64_t* full, uint64_t* empty, uint64_t* gfullc,
-                                            uint64_t* gemptyc, uint64_t* dafull, uint64_t* dafree, uint32_t tbase,
-                                            int warp, int lane, uint32_t cta, int pair) {
+                                            uint8_t* smem, uint64_t* full, uint64_t* empty, uint64_t* dafull,
+                                            uint64_t* dafree, uint32_t tbase, int warp, int lane, uint32_t cta,
+                                            int pair) {
   const int PP = p.gc_pp, PC = p.npairs - p.gc_pp, c = pair - p.gc_pp;
   const int nW = (p.n_rb + PP - 1) / PP;
   // units u = ct * nparts + part: part 0 = d chunks [0, 2), part 1 = [2, NDC) (d > 512: the accumulator of a
   // whole 768-wide column tile exceeds TMEM); unit u belongs to consumer u mod PC in every wave
   const int nparts = p.NDC > 2 ? 2 : 1, nunits = p.n_ct * nparts;
-  uint8_t* gbuf = smem;          // 2 G buffers of 32 KB: boxes (ib, jb) at (2 ib + jb) * 8 KB
-  uint8_t* sI = smem + 2 * 32768;  // n_stages_c ring stages of 32 KB (two 128-row x 64-feature boxes)
   const int nsc = p.n_stages_c;
   if (warp == kWarpTMA) {
     if (lane == 0) {
       WaitClock<DBG> wc(p.dbg, true);
-      int stage = 0, gb = 0;
-      uint32_t ph = 0, gph = 0;
+      const uint64_t polG = (p.gc_hint & 1) ? policy_evict_first() : policy_evict_normal();
+      const uint64_t polA = (p.gc_hint & 4) ? policy_evict_last() : policy_evict_normal();
+      int stage = 0;
+      uint32_t ph = 0;
+      auto acquire = [&]() -> uint8_t* {
+        wc.wait(&empty[stage], ph ^ 1u, 1);
+        if (cta == 0) mbar_arrive_expect_tx(&full[stage], 2 * 32768);
+        return smem + stage * 32768;
+      };
+      auto advance = [&]() {
+        if (++stage == nsc) {
+          stage = 0;
+          ph ^= 1;
+        }
+      };
       for (int w = 0; w < nW; ++w) {
         const int nt = min(PP, p.n_rb - w * PP);
         for (int un = c; un < nunits; un += PC) {
@@ -87,30 +100,34 @@ __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtens
           if (DBG) wc.acc[0] += clock64() - t_sp;
           fence_proxy_async_global();
           const int slot_row = (int)((g % p.gc_ring) * PP) * kRowsPerPair;
+          // the unit's dB rows (its 128 columns j of this CTA, whole rows) are pulled into L2 a few tiles before
+          // the drain: a wave-old dB tile has left L2, and the drain's reductions would wait on HBM
+          const int t_pf = max(0, nt - 12);
           for (int t = 0; t < nt; ++t) {
-            wc.wait(&gemptyc[gb], ((gph >> gb) & 1u) ^ 1u, 2);
-            gph ^= 1u << gb;
-            if (cta == 0) mbar_arrive_expect_tx(&gfullc[gb], 2 * 32768);
-            uint8_t* gd = gbuf + gb * 32768;
+            if (t == t_pf) {
+              const int j0 = ct * kColsPerTile + (int)cta * 128, nj = min(128, p.ncols - j0);
+              if (nj > 0) {
+                const char* base = reinterpret_cast<const char*>(p.dB + (long long)j0 * p.ld_dB);
+                const long long bytes = (long long)nj * p.ld_dB * 4;
+                for (long long o = 0; o < bytes; o += 65536)
+                  prefetch_l2_bulk(base + o, (uint32_t)std::min<long long>(65536, bytes - o));
+              }
+            }
+            uint8_t* gd = acquire();  // G stage: boxes (ib, jb) at (2 ib + jb) * 8 KB
 #pragma unroll
             for (int ib = 0; ib < 2; ++ib)
 #pragma unroll
               for (int jb = 0; jb < 2; ++jb)
-                tma_load_2d_pair(gd + (2 * ib + jb) * kBox, tmG, &gfullc[gb], ((int)cta * 2 + jb) * 64,
-                                 slot_row + t * kRowsPerPair + ib * 64);
-            gb ^= 1;
+                tma_load_2d_pair_hint(gd + (2 * ib + jb) * kBox, tmG, &full[stage], ((int)cta * 2 + jb) * 64,
+                                      slot_row + t * kRowsPerPair + ib * 64, polG);
+            advance();
             const int r0 = (w * PP + t) * kRowsPerPair;
             for (int tc = tc0; tc < tc1; ++tc) {
-              wc.wait(&empty[stage], ph ^ 1u, 1);
-              if (cta == 0) mbar_arrive_expect_tx(&full[stage], 2 * 32768);
-              uint8_t* dst = sI + stage * 32768;
+              uint8_t* dst = acquire();  // this CTA's 128 features of chunk tc x the tile's 128 rows
               const int d0 = tc * 256 + (int)cta * 128;
-              tma_load_2d_pair(dst, tmI, &full[stage], d0, r0);
-              tma_load_2d_pair(dst + kBoxB, tmI, &full[stage], d0 + 64, r0);
-              if (++stage == nsc) {
-                stage = 0;
-                ph ^= 1;
-              }
+              tma_load_2d_pair_hint(dst, tmI, &full[stage], d0, r0, polA);
+              tma_load_2d_pair_hint(dst + kBoxB, tmI, &full[stage], d0 + 64, r0, polA);
+              advance();
             }
           }
         }
@@ -122,8 +139,14 @@ __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtens
       WaitClock<DBG> wc(p.dbg, lane == 0);
       const unsigned long long t_loop = DBG ? clock64() : 0ull;
       const uint32_t idT = idesc_bf16(256, 256, 1, 1);
-      int stage = 0, gb = 0;
-      uint32_t ph = 0, gph = 0, dph = 0;
+      int stage = 0;
+      uint32_t ph = 0, dph = 0;
+      auto advance = [&]() {
+        if (++stage == nsc) {
+          stage = 0;
+          ph ^= 1;
+        }
+      };
       for (int w = 0; w < nW; ++w) {
         const int nt = min(PP, p.n_rb - w * PP);
         for (int un = c; un < nunits; un += PC) {
@@ -133,26 +156,23 @@ __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtens
           dph ^= 1;
           tc_fence_after();
           for (int t = 0; t < nt; ++t) {
-            wc.wait(&gfullc[gb], (gph >> gb) & 1u, 4);
-            gph ^= 1u << gb;
+            const int gs = stage;
+            wc.wait(&full[gs], ph, 4);
             tc_fence_after();
             // every G tile of step g is in smem now: the ring slot may be refilled
             if (t == nt - 1 && lane == 0) red_release_gpu_add(p.g_consumed + g, 1u);
             __syncwarp();
-            const uint32_t b_lo = (uint32_t)smem_desc_sw128(smem_u32(gbuf + gb * 32768), kBox, 1024);  // LBO = jb box stride
+            const uint32_t a_lo = (uint32_t)smem_desc_sw128(smem_u32(smem + gs * 32768), kBox, 1024);  // LBO: jb
+            advance();
             for (int tc = tc0; tc < tc1; ++tc) {
               wc.wait(&full[stage], ph, 5);
               tc_fence_after();
-              const uint32_t a_lo = (uint32_t)smem_desc_sw128(smem_u32(sI + stage * 32768), kBoxB, 1024);
+              const uint32_t b_lo = (uint32_t)smem_desc_sw128(smem_u32(smem + stage * 32768), kBoxB, 1024);
               umma_stage_dT_pair(tbase + (tc - tc0) * 256, a_lo, b_lo, idT, t != 0 ? 1u : 0u);
               umma_commit_pair_mc_warp(&empty[stage], 0x3);
-              if (++stage == nsc) {
-                stage = 0;
-                ph ^= 1;
-              }
+              advance();
             }
-            umma_commit_pair_mc_warp(&gemptyc[gb], 0x3);
-            gb ^= 1;
+            umma_commit_pair_mc_warp(&empty[gs], 0x3);
           }
           umma_commit_pair_mc_warp(dafull, 0x3);
         }
@@ -161,7 +181,7 @@ __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtens
       wc.flush(6);
     }
   } else if (warp < 8) {
-    // drain: warp (q, u) holds d-rows tc*256 + cta*128 + 32q + lane, columns 128u .. 128u + 127 of the tile
+    // drain: warp (q, u) holds columns j = ct*256 + cta*128 + 32q + lane, features 128u .. 128u + 127 of each chunk
     const int q = warp & 3, u = warp >> 2;
     const float coef = p.coef_base * __ldg(p.grad);
     WaitClock<DBG> wc(p.dbg, lane == 0);
@@ -173,18 +193,21 @@ __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtens
         daph ^= 1;
         const unsigned long long t_dr = DBG ? clock64() : 0ull;
         tc_fence_after();
+        const int j = ct * kColsPerTile + (int)cta * 128 + q * 32 + lane;
+        float* dst = p.dB + (long long)j * p.ld_dB;
         for (int tc = tc0; tc < tc1; ++tc) {
-          const int d = tc * 256 + (int)cta * 128 + q * 32 + lane;
           for (int cc = 0; cc < 4; ++cc) {
             const int col0 = u * 128 + cc * 32;
             float y[32];
             tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + (tc - tc0) * 256 + col0, y);
             tmem_ld_wait();
-            if (d < p.d_out) {
-              const int j0 = ct * kColsPerTile + col0;
+            const int d0 = tc * 256 + col0;
+            if (j < p.ncols && !(DBG && (p.gc_hint & 8))) {  // hint bit 8 (debug builds): no drain (invalid dB)
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (j0 + i < p.ncols) red_add_f32(p.dB + (long long)(j0 + i) * p.ld_dB + d, coef * y[i]);
+              for (int k = 0; k < 8; ++k)
+                if (d0 + 4 * k < p.d_out)  // d_out % 8 == 0: a group of 4 is all in or all out
+                  red_add_v4_f32(dst + d0 + 4 * k, coef * y[4 * k], coef * y[4 * k + 1], coef * y[4 * k + 2],
+                                 coef * y[4 * k + 3]);
             }
           }
         }
@@ -202,7 +225,7 @@ template <bool BWD, bool DBG, bool GC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kThreads, 1)
     pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmI,
-                const __grid_constant__ KParams p) {
+                const __grid_constant__ CUtensorMap tmGs, const __grid_constant__ KParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];  // SW128 operands need 1024-B alignment
   uint8_t* smem = smem_raw;
   if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u)) __trap();  // fail loudly, never silently misalign
@@ -215,9 +238,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kT
   // of the dA accumulator (a second one where TMEM allows, d <= 512, measured 1-3 % slower: DESIGN.md perf log)
   constexpr int kNB = BWD ? 1 : 4;
   __shared__ __align__(8) uint64_t afull, afree, sfull[kNB], sfree[kNB], gready, gfree, dafull, dafree;
-  // fused backward: producer G tile written (local warps -> store warp); consumer G buffers
-  __shared__ __align__(8) uint64_t gstore, gfullc[2], gemptyc[2];
   __shared__ uint32_t tmem_base;
+  // fused backward producers: steps g <= gc_free_upto have a free ring slot; epilogue warps that wrote their tile rows
+  __shared__ long long gc_free_upto;
+  __shared__ uint32_t gc_written;
   __shared__ __align__(16) float2 xch[2][4][2][64];  // forward column partials of a group's 2 warps (x tile parity)
   __shared__ float2 rowx[4][64];                  // forward row partials of the 4 column slices
   __shared__ __align__(16) float cval[8][64];     // backward: each warp's 64 column LSEs (log2)
@@ -233,7 +257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kT
 
   if (threadIdx.x == 0) {
     // (GC: the consumer CTAs use n_stages_c ring stages of the same arrays)
-    for (int s = 0; s < (GC ? max(p.n_stages, p.n_stages_c) : p.n_stages); ++s) {
+    for (int s = 0; s < (consumer ? p.n_stages_c : p.n_stages); ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -243,26 +267,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kT
       mbar_init(&sfull[b], 1);
       mbar_init(&sfree[b], 16);  // one arrival per epilogue warp of both CTAs
     }
+    gc_free_upto = GC ? (long long)p.gc_ring - 1 : 0;
+    gc_written = 0;
     mbar_init(&gready, 16);
-    mbar_init(&gfree, GC ? 2 : 1);  // GC: the dA MMAs' commit + the store warp's read completion
+    mbar_init(&gfree, 1);
     mbar_init(&dafull, 1);
     mbar_init(&dafree, 16);
-    if (GC) {
-      mbar_init(&gstore, 8);
-      for (int b = 0; b < 2; ++b) {
-        mbar_init(&gfullc[b], 1);
-        mbar_init(&gemptyc[b], 1);
-      }
-    }
+
     fence_mbar_init();
   }
   if (warp == kWarpTMA && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (GC) {
+    if (GC && consumer) {
       tma_prefetch_desc(&tmG);
       tma_prefetch_desc(&tmI);
     }
+    if (GC && !consumer) tma_prefetch_desc(&tmGs);
   }
   if (warp == kWarpMMA) tmem_alloc<2>(&tmem_base, kTmemCols);
   tc_fence_before();
@@ -272,49 +293,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kT
 
   const unsigned long long t_start = DBG ? clock64() : 0ull;
   if (GC && consumer) {
-    gc_consumer<DBG>(&tmG, &tmI, p, smem, full, empty, gfullc, gemptyc, &dafull, &dafree, tbase, warp, lane, cta,
-                pair);
-  } else if (GC && warp == kWarpStore) {
-    // ===================================================================== G store (fused backward, both CTAs)
-    // each finished G tile (this SM's 64 rows x 256 columns, 4 SW128 boxes) goes to ring slot g % gc_ring of step
-    // g = wave * n_ct + ct once the slot's previous step has been read; gfree is released when the store has read
-    // smem, ready[g] once the global writes are complete (one step behind, so stores overlap)
+    gc_consumer<DBG>(&tmG, &tmI, p, smem, full, empty, &dafull, &dafree, tbase, warp, lane, cta, pair);
+  } else if (GC && warp == kWarpSignal) {
+    // ===================================================================== G ring signals (fused backward)
+    // one lane keeps gc_free_upto (steps whose ring slot the consumers have read; polled from g_consumed) and
+    // publishes each finished tile: once the 8 epilogue warps counted it in gc_written, ready[g] += 1 with
+    // gpu-scope release (cumulative over their writes, acquired at CTA scope)
     if (lane == 0) {
-      WaitClock<DBG> wc(p.dbg, true);
-      uint32_t stph = 0;
-      long long pend = -1;
-      for (long long it = 0; it < nk; ++it) {
-        int rb, ct;
-        S.decode(it, rb, ct);
-        const int w = rb / p.gc_pp;
-        const long long g = (long long)w * p.n_ct + ct;
-        wc.wait(&gstore, stph, 1);
-        stph ^= 1;
-        const unsigned long long t_sp = DBG ? clock64() : 0ull;
-        if (g >= p.gc_ring) spin_geq(p.g_consumed + (g - p.gc_ring), p.NDC > 2 ? 2u : 1u, 13);
-        if (DBG) wc.acc[2] += clock64() - t_sp;
-        fence_proxy_async_global();
-        const int row = (int)(((g % p.gc_ring) * p.gc_pp + (rb - w * p.gc_pp)) * kRowsPerPair) + (int)cta * 64;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) tma_store_2d(&tmG, sG + k * kBox, k * 64, row);
-        bulk_commit();
-        const unsigned long long t_rd = DBG ? clock64() : 0ull;
-        bulk_wait_read<0>();
-        if (DBG) wc.acc[3] += clock64() - t_rd;
-        mbar_arrive(&gfree);
-        if (pend >= 0) {
-          bulk_wait<1>();
-          fence_proxy_async_global();
-          red_release_gpu_add(p.g_ready + pend, 1u);
+      const uint32_t nparts = p.NDC > 2 ? 2u : 1u;
+      const long long n_steps = (long long)((p.n_rb + p.gc_pp - 1) / p.gc_pp) * p.n_ct;
+      long long fu = (long long)p.gc_ring - 1, k = 0;
+      const unsigned long long t0 = clock64();
+      unsigned long long t_last = t0;
+      while (k < nk) {
+        bool moved = false;
+        while (fu + 1 < n_steps && ld_acquire_gpu(p.g_consumed + (fu + 1 - p.gc_ring)) >= nparts) {
+          ++fu;
+          moved = true;
         }
-        pend = g;
+        if (moved) st_volatile_shared(&gc_free_upto, fu);
+        const uint32_t wr = ld_acquire_cta_shared(&gc_written);
+        while (k < nk && wr >= 8u * (uint32_t)(k + 1)) {
+          int rb, ct;
+          S.decode(k, rb, ct);
+          fence_acq_rel_gpu();
+          red_release_gpu_add(p.g_ready + (long long)(rb / p.gc_pp) * p.n_ct + ct, 1u);
+          ++k;
+          moved = true;
+        }
+        if (moved) {
+          t_last = clock64();
+        } else {
+          __nanosleep(32);
+          if (clock64() - t_last > INFCL_WATCHDOG_CYCLES) watchdog_fire(16, (uint32_t)k);
+        }
       }
-      if (pend >= 0) {
-        bulk_wait<0>();
-        fence_proxy_async_global();
-        red_release_gpu_add(p.g_ready + pend, 1u);
-      }
-      wc.flush(8);
     }
   } else if (warp == kWarpTMA) {
     // ===================================================================== TMA producer (both CTAs)
@@ -573,10 +586,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kT
             gfph ^= 1;
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) {
-              mbar_arrive_cluster(&gready, 0);
-              if (GC) mbar_arrive(&gstore);
-            }
+            if (lane == 0) mbar_arrive_cluster(&gready, 0);
           }
         } else if constexpr (!BWD) {
           // ---------------------------------------------------------- forward statistics
@@ -641,6 +651,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kT
               pk[j / 2] &= (ok0 ? 0x0000FFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
             }
           }
+          if constexpr (GC) {
+            // fused backward: before this warp rewrites its 32 rows x 64 columns of sG, its TMA store of the
+            // previous tile must have read them
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+          }
           wc.wait(&gfree, gfph ^ 1, 9);
           gfph ^= 1;
           const uint32_t gb = smem_u32(sG) + (2 * h + u) * kBox + r * 128;
@@ -650,9 +666,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kT
                          pk[c16 * 4 + 3]);
           fence_proxy_async_smem();
           __syncwarp();  // all G writes of this warp done (and cval reads before the next tile's rewrite)
-          if (lane == 0) {
-            mbar_arrive_cluster(&gready, 0);
-            if (GC) mbar_arrive(&gstore);  // the store warp copies the tile to the G ring
+          if (lane == 0) mbar_arrive_cluster(&gready, 0);
+          if constexpr (GC) {
+            // fused backward: lane 0 stores the warp's 32 x 64 G block to ring row ((g % ring) * gc_pp + t) * 128
+            // + cta * 64 + 32 rh of step g = wave * n_ct + ct once the slot is free (gc_free_upto, kept by the
+            // signal warp), and counts the previous tile's store in gc_written once it is complete; the signal warp
+            // publishes ready[g].  The epilogue never waits on a gpu-scope release or acquire.
+            if (lane == 0) {
+              const int w = rb / p.gc_pp;
+              const long long g = (long long)w * p.n_ct + ct;
+              if (g > ld_volatile_shared(&gc_free_upto)) {
+                const unsigned long long t0 = clock64();
+                while (g > ld_volatile_shared(&gc_free_upto)) {
+                  __nanosleep(64);
+                  if (clock64() - t0 > INFCL_WATCHDOG_CYCLES) watchdog_fire(13, (uint32_t)g);
+                }
+              }
+              const int grow = (int)((g % p.gc_ring) * p.gc_pp + (rb - w * p.gc_pp)) * kRowsPerPair + (int)cta * 64;
+              if (p.gc_hint & 2)
+                tma_store_2d_hint(&tmGs, sG + (2 * h + u) * kBox + rh * 4096, h * 128 + u * 64, grow + rh * 32,
+                                  policy_evict_last());
+              else
+                tma_store_2d(&tmGs, sG + (2 * h + u) * kBox + rh * 4096, h * 128 + u * 64, grow + rh * 32);
+              bulk_commit();
+              if (tile_ctr > 0) {
+                bulk_wait<1>();
+                red_release_cta_shared_add(&gc_written, 1u);
+              }
+            }
           }
         }
         ++tile_ctr;
@@ -712,6 +753,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kT
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&dafree, 0);
+      }
+    }
+    if constexpr (GC) {
+      if (lane == 0 && tile_ctr > 0) {
+        bulk_wait<0>();
+        red_release_cta_shared_add(&gc_written, 1u);
       }
     }
     wc.flush(2 + (ep & 1));
@@ -828,9 +875,11 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
     if (!q.ok || q.npairs != g.npairs || !a.gc_ws || a.gc_ws_bytes < q.bytes || !a.dB)
       return fail(INFCL_ERR_INVALID_ARG, "fused backward: no plan or workspace");
     k.gc_pp = q.pp;
+    if (const char* e = getenv("INFCL_GC_HINT")) k.gc_hint = atoi(e);
     k.gc_ring = q.ring;
     k.g_ready = reinterpret_cast<uint32_t*>(a.gc_ws);
     k.g_consumed = k.g_ready + q.n_steps;
+    k.g_ring = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(a.gc_ws) + q.ctr_bytes);
     k.dB = a.dB;
     k.ld_dB = a.ld_dB;
   }
@@ -853,12 +902,12 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.n_stages = ns;
   k.pair_commit = (ns % 2 == 0 && !getenv("INFCL_NO_PAIR_COMMIT")) ? 1 : 0;
   const size_t smem = fixed + (size_t)ns * k.stage_bytes;
-  if (GC) {  // consumers: 2 G buffers + I stages in the same dynamic smem
-    k.n_stages_c = std::min((int)((smem - 2 * 32768) / 32768), kMaxStages);
+  if (GC) {  // consumers: one ring of 32-KB stages in the same dynamic smem
+    k.n_stages_c = std::min((int)(smem / 32768), kMaxStages);
     if (k.n_stages_c < 2) return fail(INFCL_ERR_SHAPE, "fused backward: smem too small for the consumer ring");
   }
 
-  CUtensorMap tmA, tmB, tmG, tmI;
+  CUtensorMap tmA, tmB, tmG, tmI, tmGs;
   infcl_status st = make_tmap_bf16(&tmA, a.A, a.nrows, a.dk, a.ld, 64, 64);
   if (st) return st;
   if ((st = make_tmap_bf16(&tmB, a.B, a.ncols, a.dk, a.ld, 64, 128))) return st;
@@ -867,9 +916,13 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
                              (uint64_t)q.ring * q.pp * kRowsPerPair, kColsPerTile, kColsPerTile, 64, 64)))
       return st;
     if ((st = make_tmap_bf16(&tmI, a.A, a.nrows, a.dk, a.ld, 64, 128))) return st;
+    if ((st = make_tmap_bf16(&tmGs, static_cast<uint8_t*>(a.gc_ws) + q.ctr_bytes,
+                             (uint64_t)q.ring * q.pp * kRowsPerPair, kColsPerTile, kColsPerTile, 64, 32)))
+      return st;
   } else {
     tmG = tmA;
     tmI = tmA;
+    tmGs = tmA;
   }
 
   k.noepi = !GC && getenv("INFCL_DEBUG_NOEPI") != nullptr;
@@ -900,7 +953,7 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
     INFCL_CUDA_TRY(cudaMemsetAsync(a.gc_ws, 0, (size_t)2 * q.n_steps * sizeof(uint32_t), s));
   }
   cudaEvent_t e0 = profile_begin(s);
-  kern<<<dim3(2 * g.npairs), dim3(nthreads), smem, s>>>(tmA, tmB, tmG, tmI, k);
+  kern<<<dim3(2 * g.npairs), dim3(nthreads), smem, s>>>(tmA, tmB, tmG, tmI, tmGs, k);
   INFCL_CUDA_TRY(cudaGetLastError());
   profile_end(BWD ? 1 : 0, e0, s);
   if (k.tail_scratch) launch_tail_combine(k.tail_scratch, a.dA, a.ld_dA, a.nrows, a.d_out, g, s);
@@ -961,8 +1014,8 @@ void debug_report(const char* name, int npairs, cudaStream_t s, int prod_pairs) 
   if (prod_pairs == npairs) return;
   // fused backward: consumer TMA (5), consumer MMA (6), consumer drain warps (7), producer G store warp (8)
   const char* cn[4][12] = {
-      {"ready-spin", "empty", "gempty", "", "", "", "", "", "", "", "", ""},
-      {"LOOP", "", "", "dafree", "gfull", "full", "", "", "", "", "", ""},
+      {"ready-spin", "empty", "", "", "", "", "", "", "", "", "", ""},
+      {"LOOP", "", "", "dafree", "full(G)", "full(A)", "", "", "", "", "", ""},
       {"", "", "", "", "", "", "drain", "", "", "", "dafull", ""},
       {"", "gstore", "consumed-spin", "read-wait", "", "", "", "", "", "", "", ""}};
   const double norm[4] = {ncons, ncons / 2, ncons * 8, nctas};

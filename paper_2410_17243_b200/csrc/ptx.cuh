@@ -160,7 +160,39 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       : "memory");
 }
 
-// 2D tile store smem -> global (bulk async-group completion), used by the fused backward's G ring
+// L2 cache policies for the .L2::cache_hint forms below
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d_pair_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0,
+                                                      int32_t c1, uint64_t policy) {
+  uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(b), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1,
+                                                  uint64_t policy) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(policy)
+               : "memory");
+}
+// 2D tile store smem -> global (bulk async-group completion): the fused backward's G ring
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(m)),
@@ -168,7 +200,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* s
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-// at most N of this thread's most recent bulk groups still reading their smem source / still writing
+// at most N of this thread's most recent bulk groups still reading their smem source / not yet complete
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
@@ -176,6 +208,11 @@ __device__ __forceinline__ void bulk_wait_read() {
 template <int N>
 __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+// bulk prefetch of [p, p + bytes) into L2 (bytes a multiple of 16)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+               : "memory");
 }
 // order generic-proxy global accesses against async-proxy (TMA) ones
 __device__ __forceinline__ void fence_proxy_async_global() {
@@ -185,6 +222,23 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ uint32_t ld_acquire_cta_shared(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_cta_shared_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ long long ld_volatile_shared(const long long* p) {
+  long long v;
+  asm volatile("ld.volatile.shared::cta.s64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_volatile_shared(long long* p, long long v) {
+  asm volatile("st.volatile.shared::cta.s64 [%0], %1;" ::"r"(smem_u32(p)), "l"(v) : "memory");
 }
 __device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -324,10 +378,10 @@ __device__ __forceinline__ void umma_stage_dA_pair(uint32_t d_tmem, uint32_t a_l
 #undef INFCL_STEP
 #undef INFCL_MMA2
 }
-// One G tile x one 256-d chunk of the fused backward's dT GEMM (dT^T += I^T G, K = the tile's 128 rows i) in
-// a single asm block: 8 MMAs of K = 16 rows.  A (I^T, MN-major, d contiguous) advances 16 rows = 2048 B
-// (128 in the >>4 field) per MMA; B (G, MN-major, j contiguous) lives in two 16-KB row halves (i 0-63, 64-127)
-// of two 64-column boxes each, so it advances 2048 B per MMA within a half and jumps +16 KB (1024) after 4.
+// One G tile x one 256-d chunk of the fused backward's dT GEMM (dT += G^T I, M = 256 columns j, N = 256 d, K = the
+// tile's 128 rows i) in a single asm block: 8 MMAs of K = 16 rows, both operands MN-major.  A (G^T, j contiguous)
+// lives in two 16-KB row halves (i 0-63, 64-127) of two 64-column boxes each: +2048 B (128 in the >>4 field) per
+// MMA within a half, +16 KB (1024) after 4.  B (I, d contiguous) advances 16 rows = 2048 B per MMA.
 __device__ __forceinline__ void umma_stage_dT_pair(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
                                                    uint32_t accumulate) {
 #define INFCL_MMA2(P) "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, " P ";\n\t"
@@ -339,10 +393,10 @@ __device__ __forceinline__ void umma_stage_dT_pair(uint32_t d_tmem, uint32_t a_l
       INFCL_STEP("128", "128") INFCL_MMA2("t")
       INFCL_STEP("256", "256") INFCL_MMA2("t")
       INFCL_STEP("384", "384") INFCL_MMA2("t")
-      INFCL_STEP("512", "1024") INFCL_MMA2("t")
-      INFCL_STEP("640", "1152") INFCL_MMA2("t")
-      INFCL_STEP("768", "1280") INFCL_MMA2("t")
-      INFCL_STEP("896", "1408") INFCL_MMA2("t")
+      INFCL_STEP("1024", "512") INFCL_MMA2("t")
+      INFCL_STEP("1152", "640") INFCL_MMA2("t")
+      INFCL_STEP("1280", "768") INFCL_MMA2("t")
+      INFCL_STEP("1408", "896") INFCL_MMA2("t")
       "}" ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate)
       : "memory");
 #undef INFCL_STEP
@@ -437,6 +491,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void red_add_v4_f32(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 __device__ __forceinline__ void red_add_f32(float* p, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
