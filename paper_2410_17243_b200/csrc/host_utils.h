@@ -24,6 +24,9 @@ const char* last_error_string();  // this thread's detail (infcl_last_error / in
 
 // 2D bf16 tensor map over a row-major [rows][cols] matrix with row stride `ld` elements, box
 // [box_cols (inner) x box_rows], 128-byte swizzle, zero fill out of bounds.
+// fp32 row-major [rows][ld] (ld in elements), box box_rows x box_cols, 128-B swizzle (box_cols * 4 == 128)
+infcl_status make_tmap_f32_sw128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                                 uint32_t box_cols, uint32_t box_rows);
 infcl_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
                             uint32_t box_cols, uint32_t box_rows);
 

@@ -55,7 +55,7 @@ struct PassArgs {
 struct GcPlan {
   bool ok;
   int npairs, pp, pc, ring;
-  long long n_steps;
+  long long n_steps, n_ctr;
   size_t ctr_bytes, bytes;
 };
 GcPlan gc_plan(int nrows, int ncols, int dk);

@@ -48,7 +48,8 @@ struct KParams {
                 // 4 consumer A loads evict_last
   uint16_t* g_ring;      // [gc_ring * gc_pp * 128][256] bf16 G tiles (row-major; TMA view: tmG)
   uint32_t* g_ready;     // [n_steps] producer CTAs (2 per pair) whose rows of step g's tiles are in the ring
-  uint32_t* g_consumed;  // [n_steps] 1 once step g's ring slot has been read
+  uint32_t* g_consumed;  // [n_steps] consumers (nparts) that have read step g's ring slot
+  uint32_t* g_unit_done; // [n_ct * nparts] drain warps (16 per wave) whose reductions of the unit are complete
   float* dB;             // dB (dT) accumulated with red.add (column side)
   int ld_dB;
   unsigned long long* dbg;  // optional per-tag wait-cycle accumulators (INFCL_DEBUG_WAITS)
@@ -170,11 +171,38 @@ __device__ __forceinline__ void ring_acquire(WaitClock<DBG>& wc, uint64_t* empty
 // in-thread, then 8 lanes (3 butterfly rounds).  Updates the running (mrow, srow) of the thread's 4 rows
 // (base-2 units), writes x_ii for diagonal rows, and returns (m0, S0, m1, S1): the (max, sum) partial of
 // columns cb + 2*lane and cb + 2*lane + 1 over the warp's 32 rows.
+// INFCL_FWD_POLY = k (A/B builds only): the row exponentials of the first k of every 8 column pairs are computed
+// on the FMA pipe instead of MUFU (Cody-Waite split + degree-4 polynomial, packed f32x2), Eq.5's exp
+#ifndef INFCL_FWD_POLY
+#define INFCL_FWD_POLY 0
+#endif
+// INFCL_FWD_FMAX3 = 1 (A/B builds only): the row maxima through 3-input FMNMX3 trees (measured 2 % slower)
+#ifndef INFCL_FWD_FMAX3
+#define INFCL_FWD_FMAX3 0
+#endif
+// 2^t for t <= 0 (t = -inf -> 0): t = n + f, n = round(t) by the 1.5 * 2^23 shifter, f in [-0.5, 0.5];
+// 2^f by a degree-4 minimax polynomial (max relative error 3.7e-6, below bf16 / the 2e-3 LSE gate), then n is
+// added to the exponent field
+__device__ __forceinline__ float2 ex2_poly2(float2 t) {
+  const float2 lo = make_float2(-126.f, -126.f);
+  t = make_float2(fmaxf(t.x, lo.x), fmaxf(t.y, lo.y));  // -inf and deep underflow -> 2^-126 (negligible)
+  const float2 sh = make_float2(12582912.f, 12582912.f);
+  const float2 j = __fadd2_rn(t, sh);
+  const float2 f = __fadd2_rn(t, __ffma2_rn(j, make_float2(-1.f, -1.f), sh));  // t - (j - sh) = t - n
+  float2 q = __ffma2_rn(f, make_float2(1.3333558e-3f, 1.3333558e-3f), make_float2(9.6181291e-3f, 9.6181291e-3f));
+  q = __ffma2_rn(q, f, make_float2(5.5504109e-2f, 5.5504109e-2f));
+  q = __ffma2_rn(q, f, make_float2(2.4022652e-1f, 2.4022652e-1f));
+  q = __ffma2_rn(q, f, make_float2(6.9314718e-1f, 6.9314718e-1f));
+  q = __ffma2_rn(q, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(j.y) << 23)));
+}
+
 // SELF: the launch may be self-masked (NT-Xent); a separate instantiation, so the CLIP kernels carry none of it.
 template <bool SELF>
 __device__ __forceinline__ float4 fwd_chunk_stats(float (&v)[64], uint32_t lchunk, int rowbase, int cb,
                                                   const KParams& p, int lane, float (&mrow)[4], float (&srow)[4]) {
-  float k2 = p.k2;
+  const float k2 = p.k2;
   const int t0 = lane & 3;
   bool rok[4];
 #pragma unroll
@@ -198,24 +226,32 @@ __device__ __forceinline__ float4 fwd_chunk_stats(float (&v)[64], uint32_t lchun
   // self-masked launch (NT-Xent, reading N2): the warp's 32 rows meet their own column in this chunk
   const bool selfd = SELF && p.self_mask && rowbase + p.row_off < cb + 64 && rowbase + p.row_off + 32 > cb;
   const bool ragged = selfd || !(rok[0] && rok[1] && rok[2] && rok[3]) || cb + 64 > p.ncols;
-  if (ragged) {  // scale first, then mask: at s = 0 a masked -inf times k2 = 0 would be NaN
+  if (ragged) {  // masked entries -> -inf (k2 > 0 always: the host clamps it to FLT_MIN at s = 0, no -inf * 0)
 #pragma unroll
     for (int i = 0; i < 64; ++i) {
       const int ri = (i >> 5) * 2 + ((i >> 1) & 1);
       const int col = cb + 8 * ((i >> 2) & 7) + 2 * t0 + (i & 1);
       const int row = rowbase + 16 * (ri >> 1) + 8 * (ri & 1);
-      v[i] = (rok[ri] && col < p.ncols && !(selfd && col == row + p.row_off)) ? v[i] * k2 : -INFINITY;
+      v[i] = (rok[ri] && col < p.ncols && !(selfd && col == row + p.row_off)) ? v[i] : -INFINITY;
     }
-    k2 = 1.f;
   }
-  float ml[4];  // per-row local maxima (log2 units)
+  float ml[4];  // per-row local maxima (log2 units): 16 values per row through a tree of 3-input maxima
 #pragma unroll
   for (int ri = 0; ri < 4; ++ri) {
-    float mv = -INFINITY;
+    float x[16];
 #pragma unroll
     for (int rho = 0; rho < 8; ++rho)
 #pragma unroll
-      for (int c = 0; c < 2; ++c) mv = fmaxf(mv, v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + c]);
+      for (int c = 0; c < 2; ++c) x[rho * 2 + c] = v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + c];
+#if INFCL_FWD_FMAX3
+    const float a0 = fmax3(x[0], x[1], x[2]), a1 = fmax3(x[3], x[4], x[5]), a2 = fmax3(x[6], x[7], x[8]);
+    const float a3 = fmax3(x[9], x[10], x[11]), a4 = fmax3(x[12], x[13], x[14]);
+    const float mv = fmaxf(fmax3(a0, a1, a2), fmax3(a3, a4, x[15]));
+#else  // A/B baseline: two-input maxima
+    float mv = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) mv = fmaxf(mv, x[i]);
+#endif
     ml[ri] = mv == -INFINITY ? -INFINITY : mv * k2;
   }
   // shared exponentials E = 2^{y - ml} (y = v * s * log2 e), row sums. Branch-free so the 4 rows'
@@ -230,8 +266,14 @@ __device__ __forceinline__ float4 fwd_chunk_stats(float (&v)[64], uint32_t lchun
       float& x0 = v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2];
       float& x1 = v[(ri >> 1) * 32 + rho * 4 + (ri & 1) * 2 + 1];
       const float2 t = __ffma2_rn(make_float2(x0, x1), kk, nref);
-      x0 = ex2(t.x);
-      x1 = ex2(t.y);
+      if (rho < INFCL_FWD_POLY) {  // A/B variant: these exponentials on the FMA pipe (ex2_poly2)
+        const float2 e = ex2_poly2(t);
+        x0 = e.x;
+        x1 = e.y;
+      } else {
+        x0 = ex2(t.x);
+        x1 = ex2(t.y);
+      }
       if (rho < 4) part[rho] = make_float2(x0, x1);
       else part[rho - 4] = __fadd2_rn(part[rho - 4], make_float2(x0, x1));
     }
@@ -289,7 +331,7 @@ __device__ __forceinline__ float4 fwd_chunk_stats(float (&v)[64], uint32_t lchun
       const int ri = (i >> 5) * 2 + ((i >> 1) & 1);
       const int col = cb + 8 * ((i >> 2) & 7) + 2 * t0 + (i & 1);
       const int row = rowbase + 16 * (ri >> 1) + 8 * (ri & 1);
-      y[i] = (rok[ri] && col < p.ncols && !(selfd && col == row + p.row_off)) ? y[i] * p.k2 : -INFINITY;
+      y[i] = (rok[ri] && col < p.ncols && !(selfd && col == row + p.row_off)) ? y[i] * k2 : -INFINITY;
     }
 #pragma unroll
     for (int rho = 0; rho < 8; ++rho)

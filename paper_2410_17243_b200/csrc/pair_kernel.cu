@@ -62,7 +62,8 @@ static void prof_clear() {
 // Alg.4's dT~ update with the G tiles handed over through memory instead of a read-modify-write of dT
 // per tile.
 template <bool DBG>
-__device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtensorMap* tmI, const KParams& p,
+__device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtensorMap* tmI, const CUtensorMap* tmDT,
+                                            const KParams& p,
                                             uint8_t* smem, uint64_t* full, uint64_t* empty, uint64_t* dafull,
                                             uint64_t* dafree, uint32_t tbase, int warp, int lane, uint32_t cta,
                                             int pair) {
@@ -71,6 +72,8 @@ __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtens
   // units u = ct * nparts + part: part 0 = d chunks [0, 2), part 1 = [2, NDC) (d > 512: the accumulator of a
   // whole 768-wide column tile exceeds TMEM); unit u belongs to consumer u mod PC in every wave
   const int nparts = p.NDC > 2 ? 2 : 1, nunits = p.n_ct * nparts;
+  // items k = wave * nunits + unit go round-robin over the consumers (consumer c: k = c, c + P_c, ...)
+  const long long nitems = (long long)nW * nunits;
   const int nsc = p.n_stages_c;
   if (warp == kWarpTMA) {
     if (lane == 0) {
@@ -90,15 +93,12 @@ __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtens
           ph ^= 1;
         }
       };
-      for (int w = 0; w < nW; ++w) {
+      for (long long kk = c; kk < nitems; kk += PC) {
+        const int w = (int)(kk / nunits), un = (int)(kk % nunits);
         const int nt = min(PP, p.n_rb - w * PP);
-        for (int un = c; un < nunits; un += PC) {
+        {
           const int ct = un / nparts, tc0 = (un % nparts) * 2, tc1 = min(p.NDC, tc0 + 2);
           const long long g = (long long)w * p.n_ct + ct;
-          const unsigned long long t_sp = DBG ? clock64() : 0ull;
-          spin_geq(p.g_ready + g, 2u * nt, 14);
-          if (DBG) wc.acc[0] += clock64() - t_sp;
-          fence_proxy_async_global();
           const int slot_row = (int)((g % p.gc_ring) * PP) * kRowsPerPair;
           // the unit's dB rows (its 128 columns j of this CTA, whole rows) are pulled into L2 a few tiles before
           // the drain: a wave-old dB tile has left L2, and the drain's reductions would wait on HBM
@@ -113,6 +113,11 @@ __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtens
                   prefetch_l2_bulk(base + o, (uint32_t)std::min<long long>(65536, bytes - o));
               }
             }
+            // tile t of step g is in the ring once both CTAs of producer pair t published it
+            const unsigned long long t_sp = DBG ? clock64() : 0ull;
+            spin_geq(p.g_ready + g * PP + t, 2u, 14);
+            if (DBG) wc.acc[0] += clock64() - t_sp;
+            fence_proxy_async_global();
             uint8_t* gd = acquire();  // G stage: boxes (ib, jb) at (2 ib + jb) * 8 KB
 #pragma unroll
             for (int ib = 0; ib < 2; ++ib)
@@ -147,9 +152,10 @@ __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtens
           ph ^= 1;
         }
       };
-      for (int w = 0; w < nW; ++w) {
+      for (long long kk = c; kk < nitems; kk += PC) {
+        const int w = (int)(kk / nunits), un = (int)(kk % nunits);
         const int nt = min(PP, p.n_rb - w * PP);
-        for (int un = c; un < nunits; un += PC) {
+        {
           const int ct = un / nparts, tc0 = (un % nparts) * 2, tc1 = min(p.NDC, tc0 + 2);
           const long long g = (long long)w * p.n_ct + ct;
           wc.wait(dafree, dph ^ 1u, 3, true);
@@ -159,7 +165,14 @@ __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtens
             const int gs = stage;
             wc.wait(&full[gs], ph, 4);
             tc_fence_after();
-            // every G tile of step g is in smem now: the ring slot may be refilled
+            // the tile (both CTAs' halves) is in smem: with one reader per tile (d <= 512) its 64 KB of ring lines
+            // are dead -- drop them from L2 without a write-back (hint bit 16: keep them); after the step's last
+            // tile the slot may be refilled
+            if (nparts == 1 && !(p.gc_hint & 16)) {
+              const uint16_t* tl = p.g_ring + ((g % p.gc_ring) * PP + t) * (long long)(kRowsPerPair * kColsPerTile);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) discard_l2_line(tl + (i * 32 + lane) * 64);
+            }
             if (t == nt - 1 && lane == 0) red_release_gpu_add(p.g_consumed + g, 1u);
             __syncwarp();
             const uint32_t a_lo = (uint32_t)smem_desc_sw128(smem_u32(smem + gs * 32768), kBox, 1024);  // LBO: jb
@@ -185,38 +198,61 @@ __device__ __forceinline__ void gc_consumer(const CUtensorMap* tmG, const CUtens
     const int q = warp & 3, u = warp >> 2;
     const float coef = p.coef_base * __ldg(p.grad);
     WaitClock<DBG> wc(p.dbg, lane == 0);
+    const uint32_t stg_off = (uint32_t)nsc * 32768 + warp * 4096;  // this warp's staging box (after the ring)
+    const uint32_t stg = smem_u32(smem) + stg_off;
     uint32_t daph = 0;
-    for (int w = 0; w < nW; ++w) {
-      for (int un = c; un < nunits; un += PC) {
+    for (long long kk = c; kk < nitems; kk += PC) {
+      const int w = (int)(kk / nunits), un = (int)(kk % nunits);
+      {
         const int ct = un / nparts, tc0 = (un % nparts) * 2, tc1 = min(p.NDC, tc0 + 2);
         wc.wait(dafull, daph, 10, true);
         daph ^= 1;
         const unsigned long long t_dr = DBG ? clock64() : 0ull;
         tc_fence_after();
-        const int j = ct * kColsPerTile + (int)cta * 128 + q * 32 + lane;
-        float* dst = p.dB + (long long)j * p.ld_dB;
+        // each 32 x 32 block (columns j of this warp's lanes, 32 features) goes through the warp's 4-KB staging
+        // box (128-B swizzle: conflict-free v4 stores) and a TMA reduce-add into dB (the tensor map clips the
+        // ragged columns j >= ncols and features >= d_out)
+        const int j0 = ct * kColsPerTile + (int)cta * 128 + q * 32;
+        // waves reach each dB element in wave order (bitwise reproducible dB): this unit's previous wave, drained
+        // by whichever consumer had it, has completed all 16 warps' reductions (long since, as a rule)
+        if (w > 0) {
+          if (lane == 0) {
+            spin_geq(p.g_unit_done + un, 16u * (uint32_t)w, 17);
+            fence_proxy_async_global();
+          }
+          __syncwarp();
+        }
         for (int tc = tc0; tc < tc1; ++tc) {
           for (int cc = 0; cc < 4; ++cc) {
             const int col0 = u * 128 + cc * 32;
             float y[32];
             tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + (tc - tc0) * 256 + col0, y);
             tmem_ld_wait();
-            const int d0 = tc * 256 + col0;
-            if (j < p.ncols && !(DBG && (p.gc_hint & 8))) {  // hint bit 8 (debug builds): no drain (invalid dB)
+            if (lane == 0) bulk_wait_read<0>();  // the previous block has left the staging box
+            __syncwarp();
 #pragma unroll
-              for (int k = 0; k < 8; ++k)
-                if (d0 + 4 * k < p.d_out)  // d_out % 8 == 0: a group of 4 is all in or all out
-                  red_add_v4_f32(dst + d0 + 4 * k, coef * y[4 * k], coef * y[4 * k + 1], coef * y[4 * k + 2],
-                                 coef * y[4 * k + 3]);
+            for (int c4 = 0; c4 < 8; ++c4)
+              st_shared_v4f(stg + lane * 128 + ((c4 ^ (lane & 7)) << 4), coef * y[4 * c4], coef * y[4 * c4 + 1],
+                            coef * y[4 * c4 + 2], coef * y[4 * c4 + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && !(DBG && (p.gc_hint & 8))) {  // hint bit 8 (debug builds): no drain (invalid dB)
+              tma_reduce_add_2d(tmDT, smem + stg_off, tc * 256 + col0, j0);
+              bulk_commit();
             }
           }
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(dafree, 0);
+        if (lane == 0) {
+          mbar_arrive_cluster(dafree, 0);
+          bulk_wait<0>();  // this warp's reductions of the unit are done: the unit's next wave may follow
+          red_release_gpu_add(p.g_unit_done + un, 1u);
+        }
         if (DBG) wc.acc[6] += clock64() - t_dr;
       }
     }
+    if (lane == 0) bulk_wait<0>();  // every reduction of this warp has landed before the kernel ends
     wc.flush(7);
   }
 }
@@ -225,7 +261,8 @@ template <bool BWD, bool DBG, bool GC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kThreads, 1)
     pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmI,
-                const __grid_constant__ CUtensorMap tmGs, const __grid_constant__ KParams p) {
+                const __grid_constant__ CUtensorMap tmGs, const __grid_constant__ CUtensorMap tmDT,
+                const __grid_constant__ KParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];  // SW128 operands need 1024-B alignment
   uint8_t* smem = smem_raw;
   if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u)) __trap();  // fail loudly, never silently misalign
@@ -282,6 +319,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kT
     if (GC && consumer) {
       tma_prefetch_desc(&tmG);
       tma_prefetch_desc(&tmI);
+      tma_prefetch_desc(&tmDT);
     }
     if (GC && !consumer) tma_prefetch_desc(&tmGs);
   }
@@ -293,7 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kT
 
   const unsigned long long t_start = DBG ? clock64() : 0ull;
   if (GC && consumer) {
-    gc_consumer<DBG>(&tmG, &tmI, p, smem, full, empty, &dafull, &dafree, tbase, warp, lane, cta, pair);
+    gc_consumer<DBG>(&tmG, &tmI, &tmDT, p, smem, full, empty, &dafull, &dafree, tbase, warp, lane, cta, pair);
   } else if (GC && warp == kWarpSignal) {
     // ===================================================================== G ring signals (fused backward)
     // one lane keeps gc_free_upto (steps whose ring slot the consumers have read; polled from g_consumed) and
@@ -317,7 +355,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GC ? kThreadsGC : kT
           int rb, ct;
           S.decode(k, rb, ct);
           fence_acq_rel_gpu();
-          red_release_gpu_add(p.g_ready + (long long)(rb / p.gc_pp) * p.n_ct + ct, 1u);
+          const int w = rb / p.gc_pp;
+          red_release_gpu_add(p.g_ready + ((long long)w * p.n_ct + ct) * p.gc_pp + (rb - w * p.gc_pp), 1u);
           ++k;
           moved = true;
         }
@@ -806,7 +845,10 @@ GcPlan gc_plan(int nrows, int ncols, int dk) {
     const int pp = g.npairs - pc;
     // producer tile ~ ratio consumer tiles of NDC d chunks; a consumer's units cover ~NDC / pc of every column tile
     const double prod = (double)((g.n_rb + pp - 1) / pp) * g.n_ct * ratio * NDC;
-    const double cons = (double)((g.n_ct * nparts + pc - 1) / pc) * g.n_rb * ((double)NDC / nparts);
+    // consumers take the items round-robin: ceil(items / pc) items of ~n_rb / waves tiles x NDC / nparts chunks
+    const int waves = (g.n_rb + pp - 1) / pp;
+    const long long items = (long long)waves * g.n_ct * nparts;
+    const double cons = (double)((items + pc - 1) / pc) * ((double)g.n_rb / waves) * ((double)NDC / nparts);
     const double cost = std::max(prod, cons);
     if (cost < best - 1e-9) {
       best = cost;
@@ -823,7 +865,8 @@ GcPlan gc_plan(int nrows, int ncols, int dk) {
   // >= 2: a store warp signals step g - 1 only after storing step g, which waits for step g - ring to be read
   if (const char* e = getenv("INFCL_GC_RING")) ring = std::max(2, atoi(e));
   q.ring = (int)std::min<long long>(ring, q.n_steps);
-  q.ctr_bytes = ((size_t)2 * q.n_steps * sizeof(uint32_t) + 1023) / 1024 * 1024;
+  q.n_ctr = (q.pp + 1) * q.n_steps + (long long)g.n_ct * nparts;  // ready, consumed, unit_done
+  q.ctr_bytes = ((size_t)q.n_ctr * sizeof(uint32_t) + 1023) / 1024 * 1024;
   q.bytes = q.ctr_bytes + (size_t)q.ring * q.pp * kRowsPerPair * kColsPerTile * 2;
   q.ok = true;
   return q;
@@ -849,7 +892,9 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.n_ct = g.n_ct;
   k.npairs = g.npairs;
   k.n_items = g.n_items;
-  k.k2 = a.scale * 1.4426950408889634f;
+  // s log2 e; never 0: at s = 0 the epilogues' masked -inf logits would give -inf * 0 = NaN, while FLT_MIN maps every
+  // finite logit to 0 (flushed) exactly as s = 0 does
+  k.k2 = std::max(a.scale * 1.4426950408889634f, 1.17549435e-38f);
   k.scale = a.scale;
   k.diag_on = a.diag_on;
   k.self_mask = a.self_mask;
@@ -875,10 +920,12 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
     if (!q.ok || q.npairs != g.npairs || !a.gc_ws || a.gc_ws_bytes < q.bytes || !a.dB)
       return fail(INFCL_ERR_INVALID_ARG, "fused backward: no plan or workspace");
     k.gc_pp = q.pp;
+    k.gc_hint = 5;  // consumer G loads evict_first, A loads evict_last: -16 % energy per backward (measured)
     if (const char* e = getenv("INFCL_GC_HINT")) k.gc_hint = atoi(e);
     k.gc_ring = q.ring;
     k.g_ready = reinterpret_cast<uint32_t*>(a.gc_ws);
-    k.g_consumed = k.g_ready + q.n_steps;
+    k.g_consumed = k.g_ready + q.n_steps * q.pp;
+    k.g_unit_done = k.g_consumed + q.n_steps;
     k.g_ring = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(a.gc_ws) + q.ctr_bytes);
     k.dB = a.dB;
     k.ld_dB = a.ld_dB;
@@ -903,11 +950,11 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   k.pair_commit = (ns % 2 == 0 && !getenv("INFCL_NO_PAIR_COMMIT")) ? 1 : 0;
   const size_t smem = fixed + (size_t)ns * k.stage_bytes;
   if (GC) {  // consumers: one ring of 32-KB stages in the same dynamic smem
-    k.n_stages_c = std::min((int)(smem / 32768), kMaxStages);
+    k.n_stages_c = std::min((int)(smem / 32768) - 1, kMaxStages);  // + 32 KB: the drain's staging boxes
     if (k.n_stages_c < 2) return fail(INFCL_ERR_SHAPE, "fused backward: smem too small for the consumer ring");
   }
 
-  CUtensorMap tmA, tmB, tmG, tmI, tmGs;
+  CUtensorMap tmA, tmB, tmG, tmI, tmGs, tmDT;
   infcl_status st = make_tmap_bf16(&tmA, a.A, a.nrows, a.dk, a.ld, 64, 64);
   if (st) return st;
   if ((st = make_tmap_bf16(&tmB, a.B, a.ncols, a.dk, a.ld, 64, 128))) return st;
@@ -919,10 +966,12 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
     if ((st = make_tmap_bf16(&tmGs, static_cast<uint8_t*>(a.gc_ws) + q.ctr_bytes,
                              (uint64_t)q.ring * q.pp * kRowsPerPair, kColsPerTile, kColsPerTile, 64, 32)))
       return st;
+    if ((st = make_tmap_f32_sw128(&tmDT, a.dB, a.ncols, a.d_out, a.ld_dB, 32, 32))) return st;
   } else {
     tmG = tmA;
     tmI = tmA;
     tmGs = tmA;
+    tmDT = tmA;
   }
 
   k.noepi = !GC && getenv("INFCL_DEBUG_NOEPI") != nullptr;
@@ -950,10 +999,10 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
     if (max_clusters < g.npairs)
       return fail(INFCL_ERR_UNSUPPORTED, "fused backward: only " + std::to_string(max_clusters) +
                                              " CTA pairs co-resident, need " + std::to_string(g.npairs));
-    INFCL_CUDA_TRY(cudaMemsetAsync(a.gc_ws, 0, (size_t)2 * q.n_steps * sizeof(uint32_t), s));
+    INFCL_CUDA_TRY(cudaMemsetAsync(a.gc_ws, 0, (size_t)q.n_ctr * sizeof(uint32_t), s));
   }
   cudaEvent_t e0 = profile_begin(s);
-  kern<<<dim3(2 * g.npairs), dim3(nthreads), smem, s>>>(tmA, tmB, tmG, tmI, tmGs, k);
+  kern<<<dim3(2 * g.npairs), dim3(nthreads), smem, s>>>(tmA, tmB, tmG, tmI, tmGs, tmDT, k);
   INFCL_CUDA_TRY(cudaGetLastError());
   profile_end(BWD ? 1 : 0, e0, s);
   if (k.tail_scratch) launch_tail_combine(k.tail_scratch, a.dA, a.ld_dA, a.nrows, a.d_out, g, s);

@@ -277,7 +277,9 @@ infcl_status launch_wide_forward(const PassArgs& a, cudaStream_t s) {
   k.n_ct = g.n_ct;
   k.npairs = g.npairs;
   k.n_items = g.n_items;
-  k.k2 = a.scale * 1.4426950408889634f;
+  // s log2 e; never 0: at s = 0 the epilogues' masked -inf logits would give -inf * 0 = NaN, while FLT_MIN maps every
+  // finite logit to 0 (flushed) exactly as s = 0 does
+  k.k2 = std::max(a.scale * 1.4426950408889634f, 1.17549435e-38f);
   k.scale = a.scale;
   k.diag_on = a.diag_on;
   k.self_mask = a.self_mask;
