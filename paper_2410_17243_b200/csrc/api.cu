@@ -309,7 +309,9 @@ struct Layout {
   long long slot_ld = 0;
   size_t off_slots, off_rparts, off_rstate, off_cstate, off_own2, off_ring_lse, off_ring_blk, off_expA, off_expB,
       off_dscr, off_tails, off_xstate, off_acc, total;
-  GcPlan gc{};  // fused single-pass backward (world 1, bf16): its ring shares the forward's column-slot region
+  GcPlan gc{};    // fused single-pass backward (world 1, bf16): its ring shares the forward's column-slot region
+  Gc3Plan gc3{};  // three-role variant (d <= 512), preferred when it applies
+  size_t gc_bytes() const { return std::max(gc.ok ? gc.bytes : (size_t)0, gc3.ok ? gc3.bytes : (size_t)0); }
 };
 
 // ring_ws: the ring's receive buffers live in the workspace (NCCL transport); the IPC transport receives
@@ -335,8 +337,11 @@ Layout make_layout(int64_t b, int d, int world, infcl_dtype dt, bool ring_ws = t
   // backward: per-pair partials of split tail row blocks (< 2P slots of 128 rows x dk fp32; any row range of the
   // pass has at most P - 1 tail row blocks), combined in pair order -> deterministic gradients
   const size_t tails_b = align_up((size_t)(2 * L.g.npairs - 1) * kRowsPerPair * L.dk * sizeof(float));
-  if (world == 1 && !L.f32) L.gc = gc_plan(L.bs, L.bs, L.dk);
-  L.off_slots = take(std::max(slots_b + tails_b, L.gc.ok ? L.gc.bytes : (size_t)0));
+  if (world == 1 && !L.f32) {
+    L.gc = gc_plan(L.bs, L.bs, L.dk);
+    L.gc3 = gc3_plan(L.bs, L.bs, L.dk);
+  }
+  L.off_slots = take(std::max(slots_b + tails_b, L.gc_bytes()));
   L.off_tails = L.off_slots + slots_b;
   // row partials: (row blocks + 2 x pairs) x rows-per-pair slots of whichever kernel runs (narrow or wide)
   const PassGeom gw = wide_geom(L.bs, L.bs);
@@ -507,7 +512,11 @@ infcl_status bwd_fused(Rank& R, float* dI, float* dT, const float* grad, cudaStr
   a.dB = dT;
   a.ld_dB = R.L.d;
   a.gc_ws = R.ws + R.L.off_slots;
-  a.gc_ws_bytes = R.L.gc.bytes;
+  a.gc_ws_bytes = R.L.gc_bytes();
+  if (R.L.gc3.ok) {
+    const infcl_status s3 = launch_bwd3(a, st);
+    if (s3 != INFCL_ERR_UNSUPPORTED) return s3;
+  }
   return launch_pair_backward_fused(a, st);
 }
 
@@ -1013,7 +1022,7 @@ static infcl_status backward_impl(infcl_comm comm, const void* I_local, const vo
   TRY(prepare_rank(R, I_local, T_local, dt, b, d, s, world, ws, st, world == 1 || ring_in_ws(comm)));
   if (world > 1) TRY(ring_setup(comm, R, rank, world));
   TRY(bwd_begin(R, row_lse, col_lse, diag, grad, dI, st));
-  if (world == 1 && R.L.gc.ok) {
+  if (world == 1 && (R.L.gc.ok || R.L.gc3.ok)) {
     diag_init(R, 1, dT, diag, row_lse, col_lse, grad, st);
     const infcl_status fs = bwd_fused(R, dI, dT, grad, st);
     if (fs == INFCL_OK) {
@@ -1205,7 +1214,7 @@ extern "C" infcl_status infcl_ntxent_backward(infcl_comm comm, const void* A_loc
   };
   // world 1, bf16: the (A, B) block's two passes as one fused single-pass launch (dA rows and dB columns)
   bool pair_done = false;
-  if (world == 1 && R.L.gc.ok) {
+  if (world == 1 && (R.L.gc.ok || R.L.gc3.ok)) {
     diag_init(R, 1, dB, pos, lse_a, lse_b, grad, st);
     const infcl_status fs = bwd_fused(R, dA, dB, grad, st);
     if (fs != INFCL_OK && fs != INFCL_ERR_UNSUPPORTED) return fs;

@@ -59,6 +59,15 @@ struct GcPlan {
   size_t ctr_bytes, bytes;
 };
 GcPlan gc_plan(int nrows, int ncols, int dk);
+// three-role fused backward (fused3.cu): producers (S, G), dI readers, dT readers; d <= 512
+struct Gc3Plan {
+  bool ok;
+  int npairs, pp, pc, ring, n_rb, n_ct;
+  long long n_steps, n_ctr;
+  size_t ctr_bytes, bytes;
+};
+Gc3Plan gc3_plan(int nrows, int ncols, int dk);
+infcl_status launch_bwd3(const PassArgs& a, cudaStream_t s);
 
 struct PassGeom {
   int n_rb, n_ct, npairs;
@@ -79,6 +88,7 @@ infcl_status launch_pair_backward_fused(const PassArgs& a, cudaStream_t s);
 cudaEvent_t profile_begin(cudaStream_t s);
 void profile_end(int kind, cudaEvent_t e0, cudaStream_t s);
 unsigned long long* debug_buffer(cudaStream_t s);  // INFCL_DEBUG_WAITS accumulators (zeroed) or nullptr
+unsigned long long* debug_buffer_ptr();             // the same buffer (10 x 16 counters), not re-zeroed
 // prod_pairs (fused backward): CTA pairs [0, prod_pairs) are producers, the rest consumers
 void debug_report(const char* name, int npairs, cudaStream_t s, int prod_pairs = -1);
 

@@ -1037,6 +1037,7 @@ static unsigned long long*& dbg_ptr() {
   static unsigned long long* b = nullptr;
   return b;
 }
+unsigned long long* debug_buffer_ptr() { return dbg_ptr(); }
 unsigned long long* debug_buffer(cudaStream_t s) {
   static const bool on = getenv("INFCL_DEBUG_WAITS") != nullptr;
   if (!on) return nullptr;

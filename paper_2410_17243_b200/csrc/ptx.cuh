@@ -416,6 +416,32 @@ __device__ __forceinline__ void umma_stage_dT_pair(uint32_t d_tmem, uint32_t a_l
 #undef INFCL_STEP
 #undef INFCL_MMA2
 }
+// One G stage (128 columns j) x one 256-feature chunk of the 3-role backward's dI GEMM (dI += G B_C, M = 256 rows,
+// N = 256 features, K = 128 j) in a single asm block: 8 MMAs of K = 16.  A (G, K-major, j contiguous) advances 32 B
+// (2 in the >>4 field) within a 64-column box and jumps to the second box (+BOX2) after 4; B (B_C, MN-major,
+// features contiguous) advances 16 rows = 2048 B (128) per MMA.
+template <int BOX2>
+__device__ __forceinline__ void umma_stage_kmn_pair(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
+                                                    uint32_t accumulate) {
+#define INFCL_MMA2(P) "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, " P ";\n\t"
+#define INFCL_STEP(DA, DB) "add.u32 al, %1, " DA ";\n\tadd.u32 bl, %2, " DB ";\n\tmov.b64 a, {al, hi};\n\tmov.b64 b, {bl, hi};\n\t"
+  asm volatile(
+      "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a, b;\n\t.reg .b32 al, bl, hi;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\tmov.b32 hi, 0x40004040;\n\t"
+      INFCL_STEP("0", "0") INFCL_MMA2("p")
+      INFCL_STEP("2", "128") INFCL_MMA2("t")
+      INFCL_STEP("4", "256") INFCL_MMA2("t")
+      INFCL_STEP("6", "384") INFCL_MMA2("t")
+      INFCL_STEP("%5", "512") INFCL_MMA2("t")
+      INFCL_STEP("%6", "640") INFCL_MMA2("t")
+      INFCL_STEP("%7", "768") INFCL_MMA2("t")
+      INFCL_STEP("%8", "896") INFCL_MMA2("t")
+      "}" ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate),
+      "n"(BOX2), "n"(BOX2 + 2), "n"(BOX2 + 4), "n"(BOX2 + 6)
+      : "memory");
+#undef INFCL_STEP
+#undef INFCL_MMA2
+}
 __device__ __forceinline__ void umma_commit_pair_mc_warp(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"

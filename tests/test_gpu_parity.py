@@ -312,3 +312,53 @@ def test_backward_bitwise_reproducible(b, d):
     for k in (1, 2):
         for x, y in zip(outs[0], outs[k]):
             assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("b,d,consumers,ring", [(4096, 512, "1", "2"), (4096, 512, "40", "2"), (3000, 768, "1", None),
+                                                (3000, 768, "23", "2"), (9000, 256, None, "2"), (19244, 512, "5", "3")])
+def test_fused_backward_splits(b, d, consumers, ring, monkeypatch):
+    """The fused single-pass backward at extreme producer / consumer splits and the smallest
+    G ring (2 steps: producers stall on every slot), incl. d = 768's two consumer parts per column tile: parity
+    and no deadlock (the kernel's watchdog would trap)."""
+    if consumers is not None:
+        monkeypatch.setenv("INFCL_GC_CONSUMERS", consumers)
+    if ring is not None:
+        monkeypatch.setenv("INFCL_GC_RING", ring)
+    I, T = make_features(b, d, seed=b + d, dist="paired")
+    check_all(I, T, 14.2857)
+
+
+def test_two_pass_backward_world1():
+    """INFCL_FUSED_BWD=0 (read once per process) restores the two-pass backward at world 1: parity in a child
+    process (the two-pass kernels also run at world > 1, in the virtual ring and in the host end-to-end entry)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_parity as t; "
+            "I, T = t.make_features(4096, 512, seed=3, dist='paired'); t.check_all(I, T, 14.2857, g=0.5); "
+            "I, T = t.make_features(2100, 712, seed=4, dist='independent'); t.check_all(I, T, 1.0); print('ok')")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, INFCL_FUSED_BWD="0")
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stdout[-2000:] + p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("b,d", [(4096, 512), (19244, 512), (9000, 256), (70000, 64)])
+def test_three_role_backward(b, d):
+    """The opt-in three-role fused backward (INFCL_BWD3=1, read once per process; producers,
+    dI readers, dT readers over the G ring) stays parity-green and bitwise reproducible, in a child process."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, torch; sys.path.insert(0, 'tests'); import test_gpu_parity as t; "
+            f"I, T = t.make_features({b}, {d}, seed=9, dist='paired'); "
+            "t.check_all(I, T, 14.2857) if I.shape[0] <= 20000 else None; "
+            "from paper_2410_17243_b200 import loss as K; Id, Td = I.cuda(), T.cuda(); g = torch.ones((), device='cuda'); "
+            f"outs = []\n"
+            f"for _ in range(2):\n"
+            f"    l, r, c, dg = K.infcl_forward(Id, Td, {b}, 14.2857); outs.append(K.infcl_backward(Id, Td, {b}, 14.2857, r, c, dg, g))\n"
+            "torch.cuda.synchronize(); assert all(torch.equal(x, y) for x, y in zip(outs[0], outs[1])); print('ok')")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, INFCL_BWD3="1")
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stdout[-2000:] + p.stderr[-2000:]
