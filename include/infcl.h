@@ -79,8 +79,9 @@ infcl_status infcl_comm_destroy(infcl_comm comm);
 
 /* IPC transport (the same ring schedule, Q13/Q14/Q15 readings; P:216-219 overlap):
  * infcl_comm_init_ipc: allocates and zeroes this rank's receive region on `device` (2 slots each of one
- *   travelling block [max_b/world][d'] bf16 (d' = 3 max_d for fp32 inputs), one column state and one LSE vector,
- *   plus a 4-KB counter page; infcl_comm_ipc_region_bytes reports its size).  The region is the one device
+ *   travelling block [max_b/world][d'] bf16 (d' = 3 max_d for fp32 inputs), one column state, one LSE vector and,
+ *   for bf16, one travelling dT partial [max_b/world][max_d] fp32 (the fused backward ring), plus a 4-KB counter
+ *   page; infcl_comm_ipc_region_bytes reports its size).  The region is the one device
  *   allocation the library owns; it is freed by infcl_comm_destroy.  2 <= world <= 64.
  * infcl_comm_ipc_handle: writes the region's 64-byte cudaIpcMemHandle_t to host memory `handle64`.
  * infcl_comm_ipc_connect: `handles` = world x 64 bytes (host), rank q's handle at offset 64 q, as gathered
@@ -100,8 +101,9 @@ size_t infcl_comm_ipc_region_bytes(infcl_comm comm);
 /* INFCL_TRANSPORT_NCCL / INFCL_TRANSPORT_IPC, or -1 for NULL */
 int infcl_comm_transport(infcl_comm comm);
 
-/* The per-rank ring schedule (host only, no device): the op list infcl_forward (which = 0) or one
- * infcl_backward pass (which = 1) executes at world > 1, as int32 records of 6 {code, a, b, c, tag, 0} (codes,
+/* The per-rank ring schedule (host only, no device): the op list infcl_forward (which = 0), one two-pass
+ * infcl_backward pass (which = 1) or the fused single-pass backward whose dT partials travel (which = 2) executes
+ * at world > 1, as int32 records of 6 {code, a, b, c, tag, 0} (codes,
  * streams and buffer references in api.cu: OP_*, RS_*, BUF_*; slot reference = 2 * kind + s).  Writes at most
  * `cap` records to `out` (may be NULL) and returns the count, or -1 for bad arguments.  tests/test_ring_schedule.py
  * replays it for n ranks under both transports' semantics to check it is race- and deadlock-free. */
@@ -128,7 +130,11 @@ infcl_status infcl_forward(infcl_comm comm, const void* I_local, const void* T_l
                            float* diag, float* loss, void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------------------------
- * infcl_backward -- Alg.3 over Alg.4: recompute each tile from the saved LSEs.
+ * infcl_backward -- Alg.3 over Alg.4: recompute each tile from the saved LSEs.  bf16 inputs: ONE fused
+ *   single pass per ring step (S, G and dI on producer SMs; dT from a global ring of G tiles on consumer SMs);
+ *   at world > 1 each block's dT partial travels with the block (Alg.3's rotating partials) and is home after n
+ *   hops.  fp32 inputs (and INFCL_FUSED_BWD=0 / INFCL_FUSED_RING=0): two passes, dI then dT, nothing but the
+ *   bf16 blocks and LSEs travels.
  *   row_lse, col_lse, diag : the forward's outputs for this rank (device fp32 [b/world])
  *   grad_loss              : device fp32 scalar g = dOut/dL (the same on every rank)
  *   dI_local, dT_local     : out [b/world][d] fp32 = g * dL/dI, g * dL/dT for this rank's rows (overwritten)

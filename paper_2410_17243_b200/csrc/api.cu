@@ -92,7 +92,8 @@ NcclApi& nccl() {
 // synchronised by stream memory operations on 32-bit counters (cuStreamWaitValue32 / cuStreamWriteValue32):
 // no SM is used by the exchange, so it overlaps the persistent pair kernels, which occupy every SM.
 namespace {
-enum XKind { XK_BLK = 0, XK_CS = 1, XK_LSE = 2, XK_N = 3 };  // travelling block, column state, LSE vector
+// travelling block, column state, LSE vector, and (fused backward ring) the travelling fp32 dT partial of the block
+enum XKind { XK_BLK = 0, XK_CS = 1, XK_LSE = 2, XK_DT = 3, XK_N = 4 };
 
 typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 struct MemOps {
@@ -233,6 +234,7 @@ extern "C" infcl_status infcl_comm_init_ipc(infcl_comm* out, int rank, int world
   c->cap[XK_BLK] = al(bs * dk * 2);
   c->cap[XK_CS] = al(bs * sizeof(float2));
   c->cap[XK_LSE] = al(bs * sizeof(float));
+  c->cap[XK_DT] = dt == INFCL_BF16 ? al(bs * (size_t)max_d * sizeof(float)) : 0;  // fused backward ring (bf16)
   size_t o = kFlagBytes;
   for (int k = 0; k < XK_N; ++k) {
     c->off[k] = o;
@@ -307,8 +309,8 @@ struct Layout {
   bool f32 = false;
   PassGeom g{};
   long long slot_ld = 0;
-  size_t off_slots, off_rparts, off_rstate, off_cstate, off_own2, off_ring_lse, off_ring_blk, off_expA, off_expB,
-      off_dscr, off_tails, off_xstate, off_acc, total;
+  size_t off_slots, off_rparts, off_rstate, off_cstate, off_own2, off_ring_lse, off_ring_blk, off_ring_dt, off_expA,
+      off_expB, off_dscr, off_tails, off_xstate, off_acc, total;
   GcPlan gc{};    // fused single-pass backward (world 1, bf16): its ring shares the forward's column-slot region
   Gc3Plan gc3{};  // three-role variant (d <= 512), preferred when it applies
   size_t gc_bytes() const { return std::max(gc.ok ? gc.bytes : (size_t)0, gc3.ok ? gc3.bytes : (size_t)0); }
@@ -337,9 +339,9 @@ Layout make_layout(int64_t b, int d, int world, infcl_dtype dt, bool ring_ws = t
   // backward: per-pair partials of split tail row blocks (< 2P slots of 128 rows x dk fp32; any row range of the
   // pass has at most P - 1 tail row blocks), combined in pair order -> deterministic gradients
   const size_t tails_b = align_up((size_t)(2 * L.g.npairs - 1) * kRowsPerPair * L.dk * sizeof(float));
-  if (world == 1 && !L.f32) {
-    L.gc = gc_plan(L.bs, L.bs, L.dk);
-    L.gc3 = gc3_plan(L.bs, L.bs, L.dk);
+  if (!L.f32) {
+    L.gc = gc_plan(L.bs, L.bs, L.dk);  // every ring step is a b_s x b_s block
+    if (world == 1) L.gc3 = gc3_plan(L.bs, L.bs, L.dk);
   }
   L.off_slots = take(std::max(slots_b + tails_b, L.gc_bytes()));
   L.off_tails = L.off_slots + slots_b;
@@ -352,6 +354,8 @@ Layout make_layout(int64_t b, int d, int world, infcl_dtype dt, bool ring_ws = t
   L.off_own2 = take((size_t)2 * L.bs * sizeof(float));
   L.off_ring_lse = take(world > 1 && ring_ws ? (size_t)2 * L.bs * sizeof(float) : 0);
   L.off_ring_blk = take(world > 1 && ring_ws ? (size_t)2 * L.bs * L.dk * 2 : 0);
+  // fused backward ring (NCCL transport): receive slots of the travelling dT partial
+  L.off_ring_dt = take(world > 1 && ring_ws && L.gc.ok ? (size_t)2 * L.bs * L.d * sizeof(float) : 0);
   L.off_expA = take(L.f32 ? (size_t)L.bs * L.dk * 2 : 0);
   L.off_expB = take(L.f32 ? (size_t)L.bs * L.dk * 2 : 0);
   L.off_dscr = take(L.f32 ? (size_t)L.bs * L.dk * sizeof(float) : 0);
@@ -402,6 +406,7 @@ struct Rank {
   float2* cstate(int i) const { return reinterpret_cast<float2*>(ws + L.off_cstate) + (size_t)i * L.bs; }
   float* own2(int i) const { return reinterpret_cast<float*>(ws + L.off_own2) + (size_t)i * L.bs; }
   float* ring_lse(int i) const { return reinterpret_cast<float*>(ws + L.off_ring_lse) + (size_t)i * L.bs; }
+  float* ring_dt(int i) const { return reinterpret_cast<float*>(ws + L.off_ring_dt) + (size_t)i * L.bs * L.d; }
   __nv_bfloat16* ring_blk(int i) const {
     return reinterpret_cast<__nv_bfloat16*>(ws + L.off_ring_blk) + (size_t)i * L.bs * L.dk;
   }
@@ -491,19 +496,30 @@ infcl_status bwd_step(Rank& R, const __nv_bfloat16* rowsA, const float* lse_rows
   return launch_pair_backward(a, st);
 }
 
+// INFCL_FUSED_RING=0 keeps the two-pass backward at world > 1 (INFCL_FUSED_BWD=0 disables every fused path)
+bool fused_ring_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("INFCL_FUSED_RING");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 // single-pass backward of the own pair (world 1, bf16): dI (rows I) and dT (columns T) from one fused launch;
 // both outputs already hold their exact diagonal terms (diag_init).  INFCL_ERR_UNSUPPORTED = not all CTA pairs
 // co-resident (the caller falls back to the two passes)
-infcl_status bwd_fused(Rank& R, float* dI, float* dT, const float* grad, cudaStream_t st) {
+infcl_status bwd_fused(Rank& R, float* dI, float* dT, const float* grad, cudaStream_t st,
+                       const __nv_bfloat16* held = nullptr, const float* held2 = nullptr, bool own = true,
+                       bool allow3 = true) {
   PassArgs a{};
   a.A = R.A;
-  a.B = R.B;
+  a.B = held ? held : R.B;
   a.nrows = a.ncols = R.L.bs;
   a.dk = a.ld = R.L.dk;
   a.scale = R.s;
-  a.diag_on = 1;
+  a.diag_on = own ? 1 : 0;
   a.lse_row2 = R.own2(0);
-  a.lse_col2 = R.own2(1);
+  a.lse_col2 = held2 ? held2 : R.own2(1);
   a.dA = dI;
   a.ld_dA = R.L.d;
   a.d_out = R.L.dk;
@@ -513,7 +529,7 @@ infcl_status bwd_fused(Rank& R, float* dI, float* dT, const float* grad, cudaStr
   a.ld_dB = R.L.d;
   a.gc_ws = R.ws + R.L.off_slots;
   a.gc_ws_bytes = R.L.gc_bytes();
-  if (R.L.gc3.ok) {
+  if (allow3 && R.L.gc3.ok) {
     const infcl_status s3 = launch_bwd3(a, st);
     if (s3 != INFCL_ERR_UNSUPPORTED) return s3;
   }
@@ -820,22 +836,74 @@ void bwd_ring_ops(int n, int r, std::vector<ROp>& o) {
   }
 }
 
+// the fused single-pass backward ring (Alg.3 P:539-558 with the dT partials rotating, as the forward's column
+// state does): at step k rank r holds block (T, c) of rank (r + k) mod n and that block's dT partial; the fused
+// launch adds this rank's dI rows and the block's dT partial (COMPUTE marks the block / LSE reads, MERGE the
+// read-modify-write of the partial, where the launch happens); the partial then moves on to rank r-1, and after
+// n steps it is back home complete (the n-th send is the hop home, reading Q15) -> FINISH copies it into dT
+void bwd_fused_ring_ops(int n, int r, std::vector<ROp>& o) {
+  o.push_back({OP_EVREC, RS_ST, 0, 0, -1});
+  o.push_back({OP_EVWAIT, RS_COMM, 0, 0, -1});
+  int32_t held = BUF_OWN, held2 = BUF_OWNL;
+  for (int k = 0; k < n; ++k) {
+    const int32_t blk = (r + k) % n;
+    if (k + 1 < n) {
+      if (k >= 1) {
+        o.push_back({OP_EVWAIT, RS_COMM, 5 + ((k - 1) & 1), 0, -1});
+        o.push_back({OP_WAITV, RS_COMM, XK_BLK, (k - 1) & 1, -1});
+        o.push_back({OP_WAITV, RS_COMM, XK_LSE, (k - 1) & 1, -1});
+      }
+      o.push_back({OP_SEND, XK_BLK, k & 1, held, blk});
+      o.push_back({OP_SEND, XK_LSE, k & 1, held2, blk});
+      o.push_back({OP_EVREC, RS_COMM, 2, 0, -1});
+    }
+    o.push_back({OP_COMPUTE, held, held2, k, blk});
+    const int32_t part = k == 0 ? BUF_OWNCS : slot_ref(XK_DT, (k - 1) & 1);
+    if (k >= 1) o.push_back({OP_WAITV, RS_ST, XK_DT, (k - 1) & 1, -1});  // the held block's partial arrived
+    o.push_back({OP_MERGE, part, 0, 0, blk});                           // the fused launch
+    o.push_back({OP_EVREC, RS_ST, 5 + (k & 1), 0, -1});
+    o.push_back({OP_EVREC, RS_ST, 1, 0, -1});
+    o.push_back({OP_EVWAIT, RS_COMM, 1, 0, -1});
+    o.push_back({OP_SEND, XK_DT, k & 1, part, blk});  // partial onward (last: the hop home)
+    if (k >= 1) o.push_back({OP_RELEASE, RS_COMM, XK_DT, (k - 1) & 1, -1});
+    if (k + 1 < n) {
+      o.push_back({OP_EVWAIT, RS_ST, 2, 0, -1});
+      o.push_back({OP_WAITV, RS_ST, XK_BLK, k & 1, -1});
+      o.push_back({OP_WAITV, RS_ST, XK_LSE, k & 1, -1});
+    }
+    if (k >= 1) {
+      o.push_back({OP_RELEASE, RS_ST, XK_BLK, (k - 1) & 1, -1});
+      o.push_back({OP_RELEASE, RS_ST, XK_LSE, (k - 1) & 1, -1});
+    }
+    held = slot_ref(XK_BLK, k & 1);
+    held2 = slot_ref(XK_LSE, k & 1);
+  }
+  o.push_back({OP_EVREC, RS_COMM, 3, 0, -1});  // every send (incl. the step-0 send of the own buffer) done
+  o.push_back({OP_EVWAIT, RS_ST, 3, 0, -1});
+  o.push_back({OP_WAITV, RS_ST, XK_DT, (n - 1) & 1, -1});  // own dT is home
+  o.push_back({OP_FINISH, slot_ref(XK_DT, (n - 1) & 1), 0, 0, r});
+  o.push_back({OP_RELEASE, RS_ST, XK_DT, (n - 1) & 1, -1});
+}
+
 // executor of a ring op list on `st` (compute) and comm's stream, with comm's transport
 struct RingCtx {
   const void* own = nullptr;   // BUF_OWN
   const void* ownl = nullptr;  // BUF_OWNL
-  float2* owncs = nullptr;     // BUF_OWNCS
+  float2* owncs = nullptr;     // BUF_OWNCS (forward)
+  void* ownpart = nullptr;     // BUF_OWNCS (fused backward ring: the own dT buffer, the step-0 partial)
   size_t bytes[XK_N] = {};
   std::function<infcl_status(int k, const void* blk, const void* lse)> compute;
   std::function<void(float2* cs)> merge;
   std::function<void(const float2* cs)> finish;
+  std::function<infcl_status(void* part)> merge_part;  // fused backward ring: the launch on the held partial
+  std::function<void(const void* part)> finish_part;
   double* acc = nullptr;
 };
 infcl_status run_ring(infcl_comm c, const std::vector<ROp>& ops, RingCtx& x, cudaStream_t st) {
   auto ptr = [&](int32_t ref) -> void* {
     if (ref == BUF_OWN) return const_cast<void*>(x.own);
     if (ref == BUF_OWNL) return const_cast<void*>(x.ownl);
-    if (ref == BUF_OWNCS) return x.owncs;
+    if (ref == BUF_OWNCS) return x.ownpart ? x.ownpart : static_cast<void*>(x.owncs);
     return ref >= 0 ? xslot(c, ref / 2, ref % 2) : nullptr;
   };
   auto strm = [&](int32_t id) { return id == RS_ST ? st : c->stream; };
@@ -852,8 +920,14 @@ infcl_status run_ring(infcl_comm c, const std::vector<ROp>& ops, RingCtx& x, cud
       case OP_WAITV: TRY(xwait(c, strm(op.a), op.b, op.c)); break;
       case OP_RELEASE: TRY(xrelease(c, strm(op.a), op.b, op.c)); break;
       case OP_COMPUTE: TRY(x.compute(op.c, ptr(op.a), op.b == BUF_NONE ? nullptr : ptr(op.b))); break;
-      case OP_MERGE: x.merge(static_cast<float2*>(ptr(op.a))); break;
-      case OP_FINISH: x.finish(static_cast<const float2*>(ptr(op.a))); break;
+      case OP_MERGE:
+        if (x.merge_part) TRY(x.merge_part(ptr(op.a)));
+        else x.merge(static_cast<float2*>(ptr(op.a)));
+        break;
+      case OP_FINISH:
+        if (x.finish_part) x.finish_part(ptr(op.a));
+        else x.finish(static_cast<const float2*>(ptr(op.a)));
+        break;
       case OP_ALLRED:
         if (x.acc) TRY(allreduce_acc(c, x.acc));  // NT-Xent's self-similarity rings reduce nothing
         break;
@@ -868,10 +942,11 @@ infcl_status run_ring(infcl_comm c, const std::vector<ROp>& ops, RingCtx& x, cud
 // The per-rank ring schedule as int32 records of 6 (code, a, b, c, tag, 0); which = 0 forward, 1 backward pass.
 // Returns the number of records (or -1 on bad arguments; records beyond `cap` are counted, not written).
 extern "C" int infcl_ring_schedule(int world, int rank, int which, int32_t* out, int cap) {
-  if (world < 2 || world > 64 || rank < 0 || rank >= world || which < 0 || which > 1) return -1;
+  if (world < 2 || world > 64 || rank < 0 || rank >= world || which < 0 || which > 2) return -1;
   std::vector<ROp> ops;
   if (which == 0) fwd_ring_ops(world, rank, ops);
-  else bwd_ring_ops(world, rank, ops);
+  else if (which == 1) bwd_ring_ops(world, rank, ops);
+  else bwd_fused_ring_ops(world, rank, ops);
   for (int i = 0; i < (int)ops.size() && i < cap && out; ++i) {
     const int32_t rec[6] = {ops[i].code, ops[i].a, ops[i].b, ops[i].c, ops[i].tag, 0};
     std::memcpy(out + 6 * (size_t)i, rec, sizeof(rec));
@@ -937,7 +1012,8 @@ infcl_status ring_setup(infcl_comm comm, const Rank& R, int rank, int world) {
     // every message of the schedule must fit its slot BEFORE anything is enqueued: a failing xsend part-way
     // through would leave the fill/release counters of the ring out of step (the next call would wait forever)
     if ((size_t)R.L.bs * R.L.dk * 2 > comm->cap[XK_BLK] || (size_t)R.L.bs * sizeof(float2) > comm->cap[XK_CS] ||
-        (size_t)R.L.bs * sizeof(float) > comm->cap[XK_LSE] || (int64_t)R.L.bs > comm->max_b / world)
+        (size_t)R.L.bs * sizeof(float) > comm->cap[XK_LSE] || (int64_t)R.L.bs > comm->max_b / world ||
+        (R.L.gc.ok && (size_t)R.L.bs * R.L.d * sizeof(float) > comm->cap[XK_DT]))
       return fail(INFCL_ERR_WORKSPACE, "shard larger than the IPC region was sized for (max_b, max_d)");
     int dev = -1;
     INFCL_CUDA_TRY(cudaGetDevice(&dev));
@@ -947,6 +1023,7 @@ infcl_status ring_setup(infcl_comm comm, const Rank& R, int rank, int world) {
       comm->nslot[XK_BLK][s] = R.ring_blk(s);
       comm->nslot[XK_CS][s] = R.cstate(1 + s);
       comm->nslot[XK_LSE][s] = R.ring_lse(s);
+      comm->nslot[XK_DT][s] = R.L.gc.ok ? R.ring_dt(s) : nullptr;
     }
   }
   return INFCL_OK;
@@ -1034,6 +1111,39 @@ static infcl_status backward_impl(infcl_comm comm, const void* I_local, const vo
     diag_init(R, 0, dI, diag, row_lse, col_lse, grad, st);  // nothing ran: the two passes start over
   }
   const size_t blk_bytes = (size_t)R.L.bs * R.L.dk * 2, lse_bytes = (size_t)R.L.bs * sizeof(float);
+  if (world > 1 && R.L.gc.ok && fused_ring_enabled()) {
+    // single pass over the ring: dI stays, the blocks' dT partials rotate (bwd_fused_ring_ops)
+    diag_init(R, 1, dT, diag, row_lse, col_lse, grad, st);
+    std::vector<ROp> ops;
+    bwd_fused_ring_ops(world, rank, ops);
+    RingCtx x;
+    x.own = R.B;
+    x.ownl = R.own2(1);
+    x.ownpart = dT;
+    x.bytes[XK_BLK] = blk_bytes;
+    x.bytes[XK_LSE] = lse_bytes;
+    x.bytes[XK_DT] = (size_t)R.L.bs * R.L.d * sizeof(float);
+    const __nv_bfloat16* cur_blk = nullptr;
+    const float* cur_lse = nullptr;
+    int cur_k = 0;
+    x.compute = [&](int k, const void* blk, const void* lse) {  // the launch happens at the partial's MERGE
+      cur_blk = static_cast<const __nv_bfloat16*>(blk);
+      cur_lse = static_cast<const float*>(lse);
+      cur_k = k;
+      return INFCL_OK;
+    };
+    x.merge_part = [&](void* part) {
+      return bwd_fused(R, dI, static_cast<float*>(part), grad, st, cur_blk, cur_lse, cur_k == 0, false);
+    };
+    x.finish_part = [&](const void* part) {
+      cudaMemcpyAsync(dT, part, x.bytes[XK_DT], cudaMemcpyDeviceToDevice, st);
+    };
+    TRY(run_ring(comm, ops, x, st));
+    if (dI_ready) INFCL_CUDA_TRY(cudaEventRecord(dI_ready, st));
+    TRY(comm_async_check(comm));
+    INFCL_CUDA_TRY(cudaGetLastError());
+    return INFCL_OK;
+  }
   for (int pass = 0; pass < 2; ++pass) {
     // pass 0: rows I (lse r), stream (T, c) -> dI;  pass 1: rows T (lse c), stream (I, r) -> dT
     const __nv_bfloat16* rows = pass == 0 ? R.A : R.B;
@@ -1301,6 +1411,39 @@ extern "C" infcl_status infcl_backward_virtual(const void* I, const void* T, inf
                   dI + (size_t)r * bs * d, st));
   }
   const size_t blk_bytes = (size_t)bs * R[0].L.dk * 2, lse_bytes = (size_t)bs * sizeof(float);
+  if (R[0].L.gc.ok && fused_ring_enabled()) {
+    // the fused ring's schedule (bwd_fused_ring_ops) on one device: rank r's step-k launch adds its dI rows and the
+    // dT partial of block (r + k) mod n -- accumulated in place in that block's dT rows, in the same step order as
+    // the travelling partial of the real ring
+    std::vector<const __nv_bfloat16*> held(world);
+    std::vector<const float*> held2(world);
+    for (int r = 0; r < world; ++r) {
+      held[r] = R[r].B;
+      held2[r] = R[r].own2(1);
+      diag_init(R[r], 1, dT + (size_t)r * bs * d, diag + (size_t)r * bs, row_lse + (size_t)r * bs,
+                col_lse + (size_t)r * bs, grad, st);
+    }
+    for (int k = 0; k < world; ++k) {
+      for (int r = 0; r < world; ++r) {
+        const int blk = (r + k) % world;
+        TRY(bwd_fused(R[r], dI + (size_t)r * bs * d, dT + (size_t)blk * bs * d, grad, st, held[r], held2[r], k == 0,
+                      false));
+      }
+      if (k + 1 < world) {
+        for (int r = 0; r < world; ++r) {
+          const int src = next_rank(r, world);
+          INFCL_CUDA_TRY(cudaMemcpyAsync(R[r].ring_blk(k & 1), held[src], blk_bytes, cudaMemcpyDeviceToDevice, st));
+          INFCL_CUDA_TRY(cudaMemcpyAsync(R[r].ring_lse(k & 1), held2[src], lse_bytes, cudaMemcpyDeviceToDevice, st));
+        }
+        for (int r = 0; r < world; ++r) {
+          held[r] = R[r].ring_blk(k & 1);
+          held2[r] = R[r].ring_lse(k & 1);
+        }
+      }
+    }
+    INFCL_CUDA_TRY(cudaGetLastError());
+    return INFCL_OK;
+  }
   for (int pass = 0; pass < 2; ++pass) {
     std::vector<const __nv_bfloat16*> held(world);
     std::vector<const float*> held2(world);

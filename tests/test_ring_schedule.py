@@ -26,7 +26,7 @@ from paper_2410_17243_b200 import _lib as L
 
 OP_EVREC, OP_EVWAIT, OP_SEND, OP_WAITV, OP_RELEASE, OP_COMPUTE, OP_MERGE, OP_FINISH, OP_ALLRED = range(1, 10)
 RS_ST, RS_COMM = 0, 1
-XK_BLK, XK_CS, XK_LSE = 0, 1, 2
+XK_BLK, XK_CS, XK_LSE, XK_DT = 0, 1, 2, 3
 BUF_OWN, BUF_OWNL, BUF_OWNCS, BUF_NONE = -1, -2, -3, -9
 
 
@@ -189,30 +189,60 @@ def simulate(n, programs, transport, rng):
         execute(*rng.choice(cands))
 
 
-def programs_for(n, calls, mutate=None):
-    """forward, dI pass, dT pass per call; repeated calls reuse the counters.  Block ids carried by slots are
-    made unique per call and pass (id + n * phase) so a later call's read of the same slot is not mistaken
-    for a pending read of the current content."""
+def programs_for(n, calls, mutate=None, fused=False):
+    """forward, dI pass, dT pass per call (fused: forward, one fused backward pass whose dT partials travel);
+    repeated calls reuse the counters.  Block ids carried by slots are made unique per call and pass
+    (id + n * phase) so a later call's read of the same slot is not mistaken for a pending read of the current
+    content."""
     progs = []
     for r in range(n):
-        f, b = schedule(n, r, 0), schedule(n, r, 1)
+        f, b = schedule(n, r, 0), schedule(n, r, 2 if fused else 1)
         if mutate:
             f, b = mutate(f), mutate(b)
         prog = []
-        for phase, ops in enumerate([f, b, b] * calls):
+        for phase, ops in enumerate(([f, b] if fused else [f, b, b]) * calls):
             prog += [(c, a, bb, cc, t + n * phase if (t >= 0 and c in (OP_SEND, OP_COMPUTE, OP_MERGE, OP_FINISH))
                       else t) for (c, a, bb, cc, t) in ops]
         progs.append(prog)
     return progs
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("transport", ["ipc", "nccl"])
 @pytest.mark.parametrize("n", [2, 3, 4, 5, 8])
-def test_ring_schedule_race_free(n, transport):
-    rng = random.Random(1000 * n + (transport == "ipc"))
-    progs = programs_for(n, calls=2)
+def test_ring_schedule_race_free(n, transport, fused):
+    """Both backward schedules: the two passes, and the fused single pass whose dT partials rotate (Alg.3)."""
+    rng = random.Random(1000 * n + (transport == "ipc") + 7 * fused)
+    progs = programs_for(n, calls=2, fused=fused)
     for _ in range(60 if n <= 4 else 25):
         simulate(n, progs, transport, rng)
+
+
+def test_fused_schedule_shape():
+    """Fused backward ring: every step computes block (r + k) mod n and read-modify-writes that block's dT partial;
+    the partial makes n hops (n - 1 onward + the hop home, as the forward's column state) and the call ends on the
+    rank's own, complete dT."""
+    for n in (2, 3, 8):
+        for r in range(n):
+            b = schedule(n, r, 2)
+            assert [op[4] for op in b if op[0] == OP_COMPUTE] == [(r + k) % n for k in range(n)]
+            assert [op[4] for op in b if op[0] == OP_MERGE] == [(r + k) % n for k in range(n)]
+            assert sum(op[0] == OP_SEND and op[1] == XK_DT for op in b) == n
+            assert sum(op[0] == OP_SEND and op[1] == XK_BLK for op in b) == n - 1
+            assert [op for op in b if op[0] == OP_FINISH][0][4] == r
+
+
+def test_checker_catches_fused_partial_race():
+    """Mutation: the fused schedule without the wait for the held block's partial (read before it arrives)."""
+    def drop(ops):
+        return [op for op in ops if not (op[0] == OP_WAITV and op[2] == XK_DT and op[1] == RS_ST)]
+    caught = 0
+    for seed in range(40):
+        try:
+            simulate(3, programs_for(3, calls=1, mutate=drop, fused=True), "ipc", random.Random(seed))
+        except Violation:
+            caught += 1
+    assert caught > 0
 
 
 def test_schedule_shape():
@@ -228,6 +258,7 @@ def test_schedule_shape():
             b = schedule(n, r, 1)
             assert sum(op[0] == OP_SEND and op[1] == XK_LSE for op in b) == n - 1
     assert L.lib().infcl_ring_schedule(1, 0, 0, None, 0) == -1
+    assert L.lib().infcl_ring_schedule(2, 0, 3, None, 0) == -1
 
 
 def test_checker_catches_forwarding_before_arrival():
