@@ -832,9 +832,16 @@ GcPlan gc_plan(int nrows, int ncols, int dk) {
     return e && atoi(e) == 0;
   }();
   const PassGeom g = pass_geom(nrows, ncols);
-  if (off || dk > kMaxD || g.npairs < 2) return q;
+  // below ~32K rows per launch the producer / consumer pipeline's fill and drain cost more than the saved S
+  // recompute (virtual ring at cfg2: n = 4 (b_s = 16384) 20.1 ms fused vs 18.5 two-pass; n = 2 (b_s = 32768)
+  // 14.9 vs 15.3); INFCL_GC_MIN_ROWS overrides (tests force the fused kernel at small shapes)
+  long long min_rows = 32768;
+  if (const char* e = getenv("INFCL_GC_MIN_ROWS")) min_rows = atoll(e);
+  if (off || dk > kMaxD || g.npairs < 2 || nrows < min_rows) return q;
   const int nparts = dk > 512 ? 2 : 1;  // consumer units per column tile (weights 2 : 1 when split)
-  double ratio = 2.5;
+  // producer tile time in consumer-chunk units x NDC: measured optima 22 consumers at d = 512 (2.5), 23-25 at
+  // d = 768 (2.0)
+  double ratio = dk > 512 ? 2.0 : 2.5;
   if (const char* e = getenv("INFCL_GC_RATIO")) ratio = std::max(0.1, atof(e));
   int best_pc = 1;
   double best = 1e300;

@@ -1,4 +1,4 @@
-"""A/B of the host end-to-end entry's forward schedule (INFCL_E2E_OLD_SCHEDULE): cfg2 loss+grads from pinned
+"""A/B of the host end-to-end entry's forward schedule (historical: INFCL_E2E_OLD_SCHEDULE existed in the round-1 build only): cfg2 loss+grads from pinned
 host buffers, interleaved rounds, median ms per call."""
 import json, os, statistics, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))

@@ -29,9 +29,11 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, b, d, s, dtype_name, outdir):
+def _worker(rank, world, port, b, d, s, dtype_name, outdir, fused=False):
     if ROOT not in sys.path:
         sys.path.insert(0, ROOT)
+    if fused:  # the fused backward ring (travelling dT partials) at these small shards too
+        os.environ["INFCL_GC_MIN_ROWS"] = "0"
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -57,14 +59,18 @@ def _worker(rank, world, port, b, d, s, dtype_name, outdir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("b,d,world,dtype_name", [(2 * 2048, 512, 2, "bf16"), (3 * 700, 64, 3, "bf16"),
-                                                  (4 * 1500, 128, 4, "bf16"), (2 * 320, 64, 2, "fp32"),
-                                                  (8 * 520, 64, 8, "bf16")])
-def test_ipc_ring_multiprocess(tmp_path, b, d, world, dtype_name):
+@pytest.mark.parametrize("b,d,world,dtype_name,fused", [(2 * 2048, 512, 2, "bf16", False), (3 * 700, 64, 3, "bf16", False),
+                                                        (4 * 1500, 128, 4, "bf16", False), (2 * 320, 64, 2, "fp32", False),
+                                                        (8 * 520, 64, 8, "bf16", False), (2 * 2048, 512, 2, "bf16", True),
+                                                        (3 * 700, 64, 3, "bf16", True), (8 * 520, 64, 8, "bf16", True),
+                                                        (4 * 1500, 768, 4, "bf16", True)])
+def test_ipc_ring_multiprocess(tmp_path, b, d, world, dtype_name, fused):
+    """fused: the single-pass backward ring whose dT partials travel (forced at these small shards; the default
+    uses it from 32K rows per rank); otherwise the two-pass backward ring."""
     import oracle
     from synth import make_features
     s = 14.2857
-    mp.start_processes(_worker, args=(world, _free_port(), b, d, s, dtype_name, str(tmp_path)), nprocs=world,
+    mp.start_processes(_worker, args=(world, _free_port(), b, d, s, dtype_name, str(tmp_path), fused), nprocs=world,
                        join=True, start_method="spawn")
     parts = [np.load(tmp_path / f"rank{q}.npz") for q in range(world)]
     I, T = make_features(b, d, seed=5, dist="paired", dtype=torch.float32 if dtype_name == "fp32" else torch.bfloat16)
