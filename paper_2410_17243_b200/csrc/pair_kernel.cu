@@ -924,7 +924,14 @@ static infcl_status launch_pair(const PassArgs& a, cudaStream_t s) {
   GcPlan q{};
   if (GC) {
     q = gc_plan(a.nrows, a.ncols, a.dk);
-    if (!q.ok || q.npairs != g.npairs || !a.gc_ws || a.gc_ws_bytes < q.bytes || !a.dB)
+    // a workspace sized for another launch shape (the host entry's row blocks) holds fewer ring steps: the ring
+    // depth only has to stay >= 2
+    if (q.ok && a.gc_ws && a.gc_ws_bytes < q.bytes && a.gc_ws_bytes > q.ctr_bytes) {
+      const size_t step_bytes = (size_t)q.pp * kRowsPerPair * kColsPerTile * 2;
+      q.ring = (int)std::min<long long>(q.ring, (long long)((a.gc_ws_bytes - q.ctr_bytes) / step_bytes));
+      q.bytes = q.ctr_bytes + (size_t)q.ring * step_bytes;
+    }
+    if (!q.ok || q.npairs != g.npairs || !a.gc_ws || a.gc_ws_bytes < q.bytes || q.ring < 2 || !a.dB)
       return fail(INFCL_ERR_INVALID_ARG, "fused backward: no plan or workspace");
     k.gc_pp = q.pp;
     k.gc_hint = 5;  // consumer G loads evict_first, A loads evict_last: -16 % energy per backward (measured)
