@@ -345,11 +345,17 @@ def run_ours(args):
     # while transferring; the exchange overlaps the kernels)
     ring = None
     if world > 1:
-        rb = (world - 1) * bs * d * 2 + world * bs * 8 + 2 * (world - 1) * (bs * d * 2 + bs * 4)
+        # forward: n-1 blocks + n column-state hops; backward: fused ring (1 launch per ring step) n-1 (block + LSE)
+        # hops + n hops of the fp32 dT partial, or the two-pass ring 2 (n-1) (block + LSE) hops
+        fused_ring = prof[1][0] / args.steps <= world
+        rb = (world - 1) * bs * d * 2 + world * bs * 8 + (
+            (world - 1) * (bs * d * 2 + bs * 4) + world * bs * d * 4 if fused_ring
+            else 2 * (world - 1) * (bs * d * 2 + bs * 4))
         hops, hop_ms = prof[2]
         hop_bytes = bs * d * 2
         per_hop = max_over_ranks(hop_ms / max(hops, 1))
-        ring = {"transport": args.transport, "bytes_per_rank_per_step": rb,
+        ring = {"transport": args.transport, "backward": "fused (dT partials travel)" if fused_ring else "two-pass",
+                "bytes_per_rank_per_step": rb,
                 "avg_gb_s": rb / (ms_step / 1e3) / 1e9, "link_peak_gb_s": 900.0,
                 "avg_frac_of_link": rb / (ms_step / 1e3) / 1e9 / 900.0,
                 # per-hop comm-stream events (infcl_profile_read kind 2) around each travelling-block transfer
