@@ -30,6 +30,11 @@ const char* infcl_diag_last_error(void);
 infcl_status infcl_probe_umma(const void* A, const void* B, int M, int N, int K, int a_mn_major, int ncta, int fmt,
                               float* out, int ncols, void* stream);
 
+/* TS layout self-test (A operand in TMEM): D (128 x 256) = A (128 x K) * B (K x 256) on a CTA pair, A bf16 [128][K]
+ * row-major (written into TMEM by the CTAs in the duplicated 2x2 layout), B bf16 [K][256] row-major (MN-major
+ * operand; mode & 1: B bf16 [256][K], K-major).  Writes the raw TMEM image out[2][128 lanes][128 columns] (fp32).  K % 64 == 0, K <= 256. */
+infcl_status infcl_probe_umma_ts(const void* A, const void* B, int K, int mode, float* out, void* stream);
+
 /* MMA issue-rate probe: one CTA (pair) issues `iters` back-to-back tcgen05.mma (bf16, K=16) of shape M x N from
  * resident smem; out_cycles (device, 2 x int64) = {issue cycles, issue-to-completion cycles}.  a_mn_major bits:
  * 0 = MN-major A, 1-4 = barrier wait + commit every G MMAs, 5-6 = concurrent TMEM-load warps, 8+ = clusters. */

@@ -64,6 +64,7 @@ DIAG_PATH = os.path.join(_HERE, "libinfcl_diag.so")
 DIAG_SIGNATURES = {
     "infcl_diag_last_error": (ctypes.c_char_p, []),
     "infcl_probe_umma": (_i, [_p, _p, _i, _i, _i, _i, _i, _i, _p, _i, _p]),
+    "infcl_probe_umma_ts": (_i, [_p, _p, _i, _i, _p, _p]),
     "infcl_probe_mma_rate": (_i, [_i, _i, _i, _i, _i, _p, _p]),
     "infcl_diag_max_clusters": (_i, [_i]),
     "infcl_diag_tma_rate": (_i, [_p, _i, _i, _i, _i, _i, _p]),

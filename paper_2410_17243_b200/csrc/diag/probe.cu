@@ -120,6 +120,97 @@ extern "C" infcl_status infcl_probe_umma(const void* A, const void* B, int M, in
   return INFCL_OK;
 }
 
+// ------------------------------------------------------------------ TS layout self-test (A in TMEM)
+// CTA pair, D (128 x 256) = A (128 x K) * B (K x 256): CTA c's 4 warps write A rows [64c, 64c+64) into TMEM
+// columns 256.. in the duplicated 2x2 layout (warp q: lanes 32q.., rows 32 (q & 1) + lane; bf16 pairs packed low
+// element first), B is TMA-loaded per CTA as its 128 N columns (two 64-wide MN-major SW128 boxes of K rows), the
+// leader issues K/16 TS MMAs into TMEM column 0, and the raw TMEM image (128 lanes x 128 columns) is dumped.
+namespace infcl {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    probe_umma_ts_kernel(const __grid_constant__ CUtensorMap tmB, const uint16_t* A, int K, int mode, float* out) {
+  const bool b_km = (mode & 1) != 0;  // B K-major ([256][K] rows, 64-wide K boxes) instead of MN-major ([K][256])
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar_full, bar_done;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t cta = cluster_ctarank();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_full, 1);
+    mbar_init(&bar_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<2>(&tmem_base, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  const uint32_t box = (uint32_t)K * 128;  // one 64-column MN-major box of K rows
+  if (threadIdx.x == 0) {
+    if (cta == 0) mbar_arrive_expect_tx(&bar_full, 2 * 2 * box);
+    if (b_km) {  // K blocks of 64: box 64 K x 128 rows (this CTA's N half) = 16 KB each
+      for (int kb = 0; kb < K / 64; ++kb) tma_load_2d_pair(smem + kb * 16384, &tmB, &bar_full, kb * 64, (int)cta * 128);
+    } else {
+      for (int h = 0; h < 2; ++h) tma_load_2d_pair(smem + h * box, &tmB, &bar_full, (int)cta * 128 + h * 64, 0);
+    }
+  }
+  {
+    const int row = (int)cta * 64 + 32 * (warp & 1) + lane;
+    for (int c0 = 0; c0 < K / 2; c0 += 32) {
+      uint32_t r[32];
+      for (int i = 0; i < 32; ++i) r[i] = (uint32_t)A[(size_t)row * K + 2 * (c0 + i)] |
+                                          ((uint32_t)A[(size_t)row * K + 2 * (c0 + i) + 1] << 16);
+      tmem_st32(tbase + ((uint32_t)(warp * 32) << 16) + 256 + c0, r);
+    }
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (cta == 0 && warp == 1) {
+    mbar_wait(&bar_full, 0);
+    tc_fence_after();
+    const uint32_t idesc = idesc_bf16(128, 256, 0, b_km ? 0 : 1);
+    for (int k = 0; k < K / 16; ++k) {
+      const uint64_t bd = b_km ? smem_desc_sw128(smem_u32(smem) + (k / 4) * 16384 + (k % 4) * 32, 16, 1024)
+                               : smem_desc_sw128(smem_u32(smem) + k * 2048, box, 1024);
+      umma_ts_pair_warp(tbase, tbase + 256 + 8 * k, bd, idesc, k > 0);
+    }
+    umma_commit_pair_mc_warp(&bar_done, 0x3);
+  }
+  mbar_wait(&bar_done, 0);
+  tc_fence_after();
+  float v[32];
+  const int l = warp * 32 + lane;
+  for (int c0 = 0; c0 < 128; c0 += 32) {
+    tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + c0, v);
+    tmem_ld_wait();
+    for (int j = 0; j < 32; ++j) out[((size_t)cta * 128 + l) * 128 + c0 + j] = v[j];
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc<2>(tbase, 512);
+}
+}  // namespace infcl
+
+extern "C" infcl_status infcl_probe_umma_ts(const void* A, const void* B, int K, int mode, float* out, void* stream) {
+  if (!A || !B || !out) return fail(INFCL_ERR_INVALID_ARG, "null pointer");
+  if (K % 64 || K > 256) return fail(INFCL_ERR_SHAPE, "probe shape");
+  CUtensorMap tb;
+  // B [K][256] row-major: box 64 features x K rows; or (mode & 1) B [256][K]: box 64 K x 128 rows
+  infcl_status st = (mode & 1) ? make_tmap_bf16(&tb, B, 256, K, K, 64, 128) : make_tmap_bf16(&tb, B, K, 256, 256, 64, K);
+  if (st) return st;
+  const size_t smem = 1024 + (size_t)4 * K * 128;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  INFCL_CUDA_TRY(cudaFuncSetAttribute(probe_umma_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  INFCL_CUDA_TRY(cudaLaunchKernelEx(&cfg, probe_umma_ts_kernel, tb, reinterpret_cast<const uint16_t*>(A), K, mode, out));
+  return INFCL_OK;
+}
+
 // ------------------------------------------------------------------ MMA issue-rate microbenchmark
 // Operands resident in smem (contents irrelevant), one thread of the leader CTA issues `iters` back-to-back
 // MMAs of the given shape, then commits; cycles per MMA are measured on the issuing SM.
@@ -466,7 +557,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   const int KC = KB / 2;
   const long long nst = (long long)tiles * KC;
   if (warp == 9 && cta == 0) {
-    const uint32_t idS = idesc_bf16(wide ? 256 : 128, 256, 0, 0);
+    const bool st = (mode & 2048) != 0;  // S^T shape: M=256 (stage rows) x N=128 (sA rows), same bytes per stage
+    const uint32_t idS = st ? idesc_bf16(256, 128, 0, 0) : idesc_bf16(wide ? 256 : 128, 256, 0, 0);
     int stage = 0;
     uint32_t ph = 0, sfph = 0;
     long long n = 0;
@@ -486,6 +578,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const uint64_t ad0 = smem_desc_sw128(smem_u32(sA + 2 * kc * (wide ? 16384 : 8192)), 16, 1024);
         const uint64_t bd0 = smem_desc_sw128(smem_u32(sB + stage * 32768), 16, 1024);
         if (wide) umma_stage_pair<true, (16384 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
+        else if (st) umma_stage_pair<true, (16384 >> 4), (8192 >> 4)>(dS, (uint32_t)bd0, (uint32_t)ad0, idS, kc != 0);
         else umma_stage_pair<true, (8192 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
         if (mode & 1024) {  // ONE commit per two stages: empty[even] covers the pair
           if (stage & 1) umma_commit_pair_mc_warp(&empty[stage - 1], 0x3);

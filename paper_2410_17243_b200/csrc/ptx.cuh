@@ -494,6 +494,57 @@ __device__ __forceinline__ void tmem_ld16x256x8(uint32_t taddr, float* v) {
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// ------------------------------------------------------------------ tcgen05: registers -> TMEM
+// 32 lanes x 32 bit, 32 consecutive columns: thread t of the warp writes lane (base+t), columns [col, col+32)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// ------------------------------------------------------------------ tcgen05: MMA with A in TMEM ("TS")
+// D[tmem] (+)= A[tmem] * B[smem]^T, CTA pair.  For M = 128 (64 rows per CTA) the A operand uses the duplicated
+// "2x2" data-path layout: lanes 0-31 and 64-95 both hold rows 0-31 of the CTA's 64, lanes 32-63 and 96-127 rows
+// 32-63; a 32-bit column holds 2 consecutive K elements (bf16), K = 16 per MMA = 8 columns.
+__device__ __forceinline__ void umma_ts_pair_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// One ring stage of the backward's dI GEMM in the TS form (dI += G B_C, M = 128 pair rows, N = 256 features, K = 128
+// columns j) in a single asm block: 8 MMAs of K = 16; A (G, bf16 in TMEM) advances 8 columns per MMA, the MN-major B
+// operand (B_C, features contiguous) 16 rows of j = 2048 B (128 in the >>4 field).  The first MMA accumulates iff
+// `accumulate`.
+__device__ __forceinline__ void umma_stage_dI_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t idesc,
+                                                      uint32_t accumulate) {
+#define INFCL_MMA2(P) "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [at], b, %3, " P ";\n\t"
+#define INFCL_STEP(DA, DB) "add.u32 at, %1, " DA ";\n\tadd.u32 bl, %2, " DB ";\n\tmov.b64 b, {bl, hi};\n\t"
+  asm volatile(
+      "{\n\t.reg .pred p, e, t;\n\t.reg .b64 b;\n\t.reg .b32 at, bl, hi;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\tmov.b32 hi, 0x40004040;\n\t"
+      INFCL_STEP("0", "0") INFCL_MMA2("p")
+      INFCL_STEP("8", "128") INFCL_MMA2("t")
+      INFCL_STEP("16", "256") INFCL_MMA2("t")
+      INFCL_STEP("24", "384") INFCL_MMA2("t")
+      INFCL_STEP("32", "512") INFCL_MMA2("t")
+      INFCL_STEP("40", "640") INFCL_MMA2("t")
+      INFCL_STEP("48", "768") INFCL_MMA2("t")
+      INFCL_STEP("56", "896") INFCL_MMA2("t")
+      "}" ::"r"(d_tmem), "r"(a_tmem), "r"(b_lo), "r"(idesc), "r"(accumulate)
+      : "memory");
+#undef INFCL_STEP
+#undef INFCL_MMA2
+}
+
 // ------------------------------------------------------------------ descriptors
 // Shared-memory matrix descriptor (sm_100 "version 1"): start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
 // version=1 [46,48), base_offset [49,52)=0, lbo_mode [52]=0, layout [61,64) (2 = SWIZZLE_128B).

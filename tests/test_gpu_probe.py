@@ -54,3 +54,23 @@ def test_pair_m128_2x2_layout():
         if not close(out[c], exp):
             # diagnostic: find for each lane which (row, col-offset) it matches
             pytest.fail(f"cta {c}: layout mismatch; out[:, :4]={out[c, ::16, :4]} ref rows={ref[::16, :4]}")
+
+
+@pytest.mark.parametrize("K", [64, 256])
+@pytest.mark.parametrize("b_km", [0, 1])
+def test_pair_m128_ts_duplicated_a(K, b_km):
+    # TS form (A in TMEM, duplicated 2x2 layout; B MN-major from smem), D in the same 2x2 layout as the SS pair M=128
+    g = torch.Generator().manual_seed(K)
+    A = torch.randn(128, K, generator=g).to(torch.bfloat16)
+    B = torch.randn(K, 256, generator=g).to(torch.bfloat16)
+    out = torch.full((2, 128, 128), float("nan"), device="cuda")
+    Bd = (B.t().contiguous() if b_km else B).cuda()
+    L.diag_call("infcl_probe_umma_ts", A.cuda().data_ptr(), Bd.data_ptr(), K, b_km, out.data_ptr(),
+                torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float()
+    out = out.cpu()
+    for c in range(2):
+        rows = ref[64 * c:64 * c + 64]
+        exp = torch.cat([rows[:, :128], rows[:, 128:]], dim=0)
+        assert close(out[c], exp), (c, out[c, ::16, :4], exp[::16, :4])
