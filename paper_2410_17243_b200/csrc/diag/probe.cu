@@ -579,6 +579,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const uint64_t bd0 = smem_desc_sw128(smem_u32(sB + stage * 32768), 16, 1024);
         if (wide) umma_stage_pair<true, (16384 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
         else if (st) umma_stage_pair<true, (16384 >> 4), (8192 >> 4)>(dS, (uint32_t)bd0, (uint32_t)ad0, idS, kc != 0);
+        else if (mode & 4096)  // TS form: A (garbage) in TMEM columns 384.., B = the stage as an MN-major operand
+          umma_stage_dI_ts_pair(dS, tbase + 384, (uint32_t)smem_desc_sw128(smem_u32(sB + stage * 32768), 16384, 1024),
+                                idesc_bf16(128, 256, 0, 1), kc != 0);
         else umma_stage_pair<true, (8192 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
         if (mode & 1024) {  // ONE commit per two stages: empty[even] covers the pair
           if (stage & 1) umma_commit_pair_mc_warp(&empty[stage - 1], 0x3);
