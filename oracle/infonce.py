@@ -198,7 +198,23 @@ def loss_and_grads(I, T, s: float, g: float = 1.0) -> dict:
 # --------------------------------------------------------------------------------------------------
 # Large-b protocol (SURVEY 8(c)): exact fp64 streamed over row chunks, sampled gradients
 # --------------------------------------------------------------------------------------------------
-def streamed_forward(I, T, s: float, chunk: int = 1024, row_limit: int | None = None) -> dict:
+def _chunk_map(fn, starts, chunk_bytes: int, workers: int = 1) -> list:
+    """[fn(i0) for i0 in starts]; with workers > 1 (the large-b parity tests' wall time) evaluated by up to that
+    many threads (numpy's exp and matmul release the GIL).  Each chunk's arithmetic is exactly the serial loop's
+    and the results come back in chunk order, so every caller combines them in the same order as a plain loop:
+    threading changes wall time only.  Workers are capped by host memory (~12 GB of chunk temporaries).  The
+    default (1) is the plain loop, which is what bench.py times as the CPU baseline."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    starts = list(starts)
+    workers = max(1, min(workers, os.cpu_count() or 1, len(starts), int(12e9 // max(1, chunk_bytes))))
+    if workers == 1:
+        return [fn(i0) for i0 in starts]
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        return list(ex.map(fn, starts))
+
+
+def streamed_forward(I, T, s: float, chunk: int = 1024, row_limit: int | None = None, workers: int = 1) -> dict:
     """Same definition as ``forward`` but X is streamed in row chunks: r per chunk, c by merging the
     chunk's column LSEs (Eq.4 merge, reading Q1/Q2).  O(chunk * b) memory; exact up to rounding.
     ``row_limit`` restricts the rows (a bounded sample of the workload for CPU timing): r and diag are
@@ -211,19 +227,25 @@ def streamed_forward(I, T, s: float, chunk: int = 1024, row_limit: int | None = 
     r = np.empty(nrows)
     diag = np.empty(nrows)
     c = np.full(T.shape[0], NEG_INF)
-    for i0 in range(0, nrows, chunk):
+
+    def one(i0):  # one row chunk of X: its row LSEs, its column LSEs (merged below in chunk order), its diagonal
         i1 = min(nrows, i0 + chunk)
         Xc = s32 * (I[i0:i1] @ T.T)
-        r[i0:i1] = tile_lse(Xc)
-        c = merge_lse(c, tile_lse(Xc.T))
-        diag[i0:i1] = Xc[np.arange(i1 - i0), np.arange(i0, i1)]
+        return tile_lse(Xc), tile_lse(Xc.T), Xc[np.arange(i1 - i0), np.arange(i0, i1)]
+
+    for i0, (rc, cc, dc) in zip(range(0, nrows, chunk),
+                                _chunk_map(one, range(0, nrows, chunk), 4 * chunk * T.shape[0] * 8, workers)):
+        i1 = min(nrows, i0 + chunk)
+        r[i0:i1] = rc
+        c = merge_lse(c, cc)
+        diag[i0:i1] = dc
     out = {"r": r, "c": c, "diag": diag}
     if row_limit is None:
         out["loss"] = 0.5 * (math.fsum(r - diag) + math.fsum(c - diag)) / b
     return out
 
 
-def streamed_grad_scale(I, T, s: float, r, c, g: float = 1.0, chunk: int = 2048) -> float:
+def streamed_grad_scale(I, T, s: float, r, c, g: float = 1.0, chunk: int = 2048, workers: int = 1) -> float:
     """g dL/ds = sum_ij G_ij <I_i, T_j> with G as in ``backward`` (x_ij = s <I_i, T_j> is linear in s, so
     dL/ds = sum_ij (dL/dx_ij) x_ij / s), streamed over row chunks of X without forming dI, dT:
     one GEMM per chunk.  r, c are the LSEs (exact ones from ``streamed_forward`` for an exact result)."""
@@ -233,15 +255,16 @@ def streamed_grad_scale(I, T, s: float, r, c, g: float = 1.0, chunk: int = 2048)
     b = I.shape[0]
     r = np.asarray(r, dtype=np.float64)
     c = np.asarray(c, dtype=np.float64)
-    acc = []
-    for i0 in range(0, b, chunk):
+    def one(i0):  # one row chunk: sum_ij G_ij P_ij over its rows
         i1 = min(b, i0 + chunk)
         P = I[i0:i1] @ T.T
         Xc = s32 * P
         G = (g / (2.0 * b)) * (np.exp(Xc - r[i0:i1, None]) + np.exp(Xc - c[None, :]))
         rows = np.arange(i0, i1)
         G[rows - i0, rows] -= g / b
-        acc.append(float((G * P).sum()))
+        return float((G * P).sum())
+
+    acc = _chunk_map(one, range(0, b, chunk), 6 * chunk * T.shape[0] * 8, workers)
     return math.fsum(acc)
 
 

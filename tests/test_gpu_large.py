@@ -44,7 +44,7 @@ def test_cfg2_full_size_random_paired():
     loss, r, c, dg = K.infcl_forward(Id, Td, b, S)
     dI, dT = K.infcl_backward(Id, Td, b, S, r, c, dg, torch.tensor(1.0, device="cuda"))
     torch.cuda.synchronize()
-    ref = oracle.streamed_forward(I, T, S, chunk=2048)
+    ref = oracle.streamed_forward(I, T, S, chunk=512, workers=8)
     assert abs(loss.item() - ref["loss"]) <= 1e-4 * abs(ref["loss"])
     assert np.abs(r.cpu().numpy() - ref["r"]).max() <= 2e-3
     assert np.abs(c.cpu().numpy() - ref["c"]).max() <= 2e-3
@@ -126,7 +126,7 @@ def test_e2e_host_entry_chunked(b, d):
     the rows on both sides of every chunk / piece boundary against the exact fp64 rows."""
     I, T = make_features(b, d, seed=11, dist="paired")
     loss, dI, dT = K.infcl_loss_grad_host(I.pin_memory(), T.pin_memory(), S)
-    ref = oracle.streamed_forward(I, T, S, chunk=4096)
+    ref = oracle.streamed_forward(I, T, S, chunk=512, workers=8)
     assert abs(loss.item() - ref["loss"]) <= 1e-4 * abs(ref["loss"])
     rows = stratified_rows(b, 96)
     rows = np.unique(np.concatenate([rows, [x for c in e2e_boundaries(b) for x in (c - 1, c)]]))
@@ -148,7 +148,7 @@ def test_wide_forward_waves_and_tail(b, d):
     loss, r, c, dg = K.infcl_forward(Id, Td, b, S)
     dI, dT = K.infcl_backward(Id, Td, b, S, r, c, dg, torch.tensor(1.0, device="cuda"))
     torch.cuda.synchronize()
-    ref = oracle.streamed_forward(I, T, S, chunk=4096)
+    ref = oracle.streamed_forward(I, T, S, chunk=512, workers=8)
     assert abs(loss.item() - ref["loss"]) <= 1e-4 * abs(ref["loss"])
     assert np.abs(r.cpu().numpy() - ref["r"]).max() <= 2e-3
     assert np.abs(c.cpu().numpy() - ref["c"]).max() <= 2e-3

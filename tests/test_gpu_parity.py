@@ -268,8 +268,8 @@ def test_grad_scale_cfg2(s, dist):
     dI, dT = K.infcl_backward(Id, Td, b, s, r, c, dg, torch.tensor(g, device="cuda"))
     ds = K.infcl_grad_scale(Id, dI, s).item()
     del dI, dT
-    f = oracle.streamed_forward(I, T, s, chunk=2048)
-    ref = oracle.streamed_grad_scale(I, T, s, f["r"], f["c"], g)
+    f = oracle.streamed_forward(I, T, s, chunk=512, workers=8)
+    ref = oracle.streamed_grad_scale(I, T, s, f["r"], f["c"], g, chunk=512, workers=8)
     tol = 2e-3 * abs(ref) + 1e-12
     assert abs(ref) > tol
     assert abs(ds - ref) <= tol, (ds, ref, abs(ds - ref) / abs(ref))

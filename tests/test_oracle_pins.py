@@ -376,3 +376,16 @@ def test_backward_abs_bounds_gradient():
     # one-hot: off-class components of dI are s*g/b*m*q >= 0 and equal their magnitude bound
     off = ~np.eye(8, dtype=bool)
     assert np.allclose(aI1[off], np.abs(cf["dI"][off]), atol=1e-15)
+
+
+def test_streamed_threads_bitwise_equal_serial():
+    """The large-b parity tests run the streamed oracle with worker threads (wall time only): every output is
+    bitwise the serial loop's (same per-chunk arithmetic, chunk-ordered combination)."""
+    g = np.random.default_rng(3)
+    I = g.standard_normal((1000, 24))
+    T = g.standard_normal((1000, 24))
+    a = oracle.streamed_forward(I, T, 3.0, chunk=96)
+    b = oracle.streamed_forward(I, T, 3.0, chunk=96, workers=4)
+    assert all(np.array_equal(a[k], b[k]) for k in ("r", "c", "diag")) and a["loss"] == b["loss"]
+    assert oracle.streamed_grad_scale(I, T, 3.0, a["r"], a["c"], 0.7, chunk=96) == \
+        oracle.streamed_grad_scale(I, T, 3.0, a["r"], a["c"], 0.7, chunk=96, workers=4)
