@@ -45,7 +45,10 @@ def max_over_ranks(x: float) -> float:
 
 # ------------------------------------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi sampled every 200 ms DURING the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampled every 50 ms DURING the timed region (B200_PROFILING.md clocks line).  Started before the
+    warm-up steps and awaited (first sample) before the timed loop: nvidia-smi's start-up takes the driver for up to
+    ~100 ms, which, inside the timed loop, stalled kernel launches and left the GPU idle (a 1.5-6.7 ms/step swing
+    between back-to-back runs).  Only samples that arrive inside the timed window are summarised."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -69,7 +72,15 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def wait_first(self, timeout: float = 10.0):
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.01)
+
+    def window(self, t0: float, t1: float):
+        self.t0, self.t1 = t0, t1
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -82,7 +93,11 @@ class ClockSampler:
     def summary(self):
         sm, mx, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        lines = [ln for (t, ln) in self.lines if t0 is None or t0 <= t <= t1 + 0.05]
+        if not lines:  # a window shorter than the sampling period: the samples around it
+            lines = [ln for (t, ln) in self.lines if t0 is None or t0 - 0.1 <= t <= t1 + 0.1]
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -245,9 +260,11 @@ def run_ours(args):
         dI, dT = K.infcl_backward(I, T, b, s, r, c, dg, g, rank, world, comm, ws)
         return loss, dI, dT
 
+    clk = ClockSampler(local).__enter__()  # before the warm-up: its start-up must not overlap the timed loop
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    clk.wait_first()
     # peak memory of ONE call (the paper's loss memory M_loss, Eq.9): outputs of earlier steps released,
     # the L2-flush buffer (a benchmark artefact) excluded; counts the I, T shards, the workspace, r, c, diag,
     # dI, dT, and the library-owned IPC receive region
@@ -264,10 +281,17 @@ def run_ours(args):
             torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     lib.infcl_reset_launch_count()
     lib.infcl_profile_enable(1)
-    with ClockSampler(local) as clk:
+    try:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        import gc
+        gc.disable()  # no collector pause while the host enqueues the timed steps
+        t_win0 = time.time()
+        # ~10 ms of device-side sleep ahead of the first step (outside every step's events): the host enqueues the
+        # timed steps meanwhile, so a host-side stall (another process polling the driver) cannot leave the GPU idle
+        # inside a step; each step's events still bracket exactly its own kernels
+        torch.cuda._sleep(int(2e7))
         for e0, e1, e2 in evs:
             flush.zero_()  # L2 flush between timed steps (outside the per-step events)
             e0.record(stream)
@@ -275,9 +299,15 @@ def run_ours(args):
             e1.record(stream)
             dI, dT = K.infcl_backward(I, T, b, s, r, c, dg, g, rank, world, comm, ws)
             e2.record(stream)
+        host_enqueue_ms = (time.time() - t_win0) * 1e3
         torch.cuda.synchronize()
+        clk.window(t_win0, time.time())
         if world > 1:
             dist.barrier()
+    finally:
+        import gc
+        gc.enable()
+        clk.__exit__(None, None, None)
     launches = int(lib.infcl_launch_count())
     import ctypes
     prof = {}
@@ -382,7 +412,7 @@ def run_ours(args):
                "config": {"workload": name, "b": b, "d": d, "logit_scale": s, "parallelism": f"ring{world}" + (f"-{args.transport}" if world > 1 else ""),
                           "l2": "512 MB buffer written between timed steps (outside per-step events)",
                           "inputs": "L2-normalised N(0,1) rows, bf16 RNE, generated on device"},
-               "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "non_kernel_ms": non_kernel_ms, "peak_gb_per_gpu": peak_gb,
+               "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "non_kernel_ms": non_kernel_ms, "host_enqueue_ms": host_enqueue_ms, "peak_gb_per_gpu": peak_gb,
                "peak_gb_accounting": "one call: I,T shards + workspace + r,c,diag + dI,dT (+ IPC region); "
                                      "outputs of earlier steps released; L2-flush buffer excluded",
                "loss": lval,
