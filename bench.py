@@ -13,6 +13,7 @@ run has) on a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -285,7 +286,6 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        import gc
         gc.disable()  # no collector pause while the host enqueues the timed steps
         t_win0 = time.time()
         # ~10 ms of device-side sleep ahead of the first step (outside every step's events): the host enqueues the
@@ -305,7 +305,6 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
     finally:
-        import gc
         gc.enable()
         clk.__exit__(None, None, None)
     launches = int(lib.infcl_launch_count())
