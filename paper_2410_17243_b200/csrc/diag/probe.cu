@@ -220,16 +220,24 @@ template <int NCTA>
 __global__ void __launch_bounds__(128, 1) probe_rate_kernel(int M, int N, int a_mn, int iters, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_done, bar_ready, bar_dummy;
+  __shared__ uint64_t bar_done, bar_ready, bar_dummy, bar_done2;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x / 32;
   const uint32_t cta = NCTA == 2 ? cluster_ctarank() : 0;
-  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3f803f80u;
+  const bool stream = (a_mn & 128) != 0;  // M=128 N=256 pair loop over the pair kernel's real footprint (192 KB)
+  const uint32_t fillv = (iters & (1 << 30)) ? 0x3c003c00u : 0x3f803f80u;  // iters bit 30: the walk probes' fill
+  // iters bit 29: the idle warps wait in the cluster barrier (as the walk probes' idle warps do) instead of on an
+  // mbarrier while the MMA warp issues
+  const bool idle_cluster_bar = (iters & (1 << 29)) != 0;
+  iters &= (1 << 29) - 1;
+  for (int i = threadIdx.x; i < (stream ? 192 : 64) * 1024 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem)[i] = fillv;
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
     mbar_init(&bar_done, 1);
     mbar_init(&bar_ready, 1);
     mbar_init(&bar_dummy, 1 << 19);
+    mbar_init(&bar_done2, 1);
     fence_mbar_init();
     mbar_arrive(&bar_ready);  // phase 0 completes: waits on it return at once
   }
@@ -266,7 +274,31 @@ __global__ void __launch_bounds__(128, 1) probe_rate_kernel(int M, int N, int a_
     const uint64_t bd0 = smem_desc_sw128(sb, 16, 1024);
     const uint64_t astep = amn ? 128 : 2;
     const long long t0 = clock64();
-    if (G == 0) {
+    if (stream) {  // A: 8 boxes of 64 rows x 128 B (64 KB), B: 4 stages of 2 boxes of 128 rows x 128 B (128 KB)
+      const uint32_t sA = smem_u32(smem), sB = smem_u32(smem + 65536);
+      // G field in this mode = loop-structure variant bits: 1 first MMA of every 4 stages overwrites (accumulate 0),
+      // 2 D rotates over 4 buffers of 128 columns every 4 stages, 4 tcgen05.fence::after_thread_sync every stage
+      // (an earlier build: D alternating between two regions every stage -- 64 cycles), 8 commit to a real
+      // (count-1) barrier every stage and a wait 3 stages back
+      const int var = G;
+      uint32_t ph = 0;
+      for (int i = 0; i < iters; i += 8) {
+        const int s8 = i >> 3, st = s8 & 3;
+        const uint32_t acc = ((var & 1) && st == 0) ? 0u : 1u;
+        uint32_t d = tbase;
+        if (var & 2) d += (uint32_t)((s8 >> 2) & 3) * 128;
+        if (var & 4) tc_fence_after();  // (variant bit 4 now: tcgen05.fence::after_thread_sync per stage)
+        umma_stage_pair<true, (8192 >> 4), (16384 >> 4)>(d, (uint32_t)smem_desc_sw128(sA + 2 * st * 8192, 16, 1024),
+                                                         (uint32_t)smem_desc_sw128(sB + st * 32768, 16, 1024), idesc, acc);
+        if (var & 8) {
+          umma_commit_pair_mc_warp(&bar_done2, 0x3);
+          if (s8 >= 3) {  // wait for the commit 3 stages back (a 4-deep ring's empty barrier)
+            mbar_wait(&bar_done2, ph);
+            ph ^= 1;
+          }
+        }
+      }
+    } else if (G == 0) {
       for (int i = 0; i < iters; i += 8) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) umma_bf16_warp<NCTA>(tbase, ad0 + (uint64_t)((k & 3) * astep), bd0 + (uint64_t)(2 * (k & 3)), idesc, 1u);
@@ -292,7 +324,7 @@ __global__ void __launch_bounds__(128, 1) probe_rate_kernel(int M, int N, int a_
     stop_flag = 1;
   }
   if (NCTA == 2 && cta != 0 && threadIdx.x == 0) stop_flag = 1;
-  if (cta != 0 || warp != 1) mbar_wait(&bar_done, 0);
+  if ((cta != 0 || warp != 1) && !idle_cluster_bar) mbar_wait(&bar_done, 0);
   tc_fence_before();
   if constexpr (NCTA == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) tmem_dealloc<NCTA>(tbase, 512);
@@ -307,7 +339,8 @@ extern "C" infcl_status infcl_probe_mma_rate(int M, int N, int a_mn_major, int n
   a_mn_major &= 0xff;
   cfg.gridDim = dim3(ncta * nclusters);
   cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = 64 * 1024 + 1024;
+  const bool stream_mode = (a_mn_major & 128) != 0;
+  cfg.dynamicSmemBytes = (stream_mode ? 192 : 64) * 1024 + 1024;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -320,7 +353,7 @@ extern "C" infcl_status infcl_probe_mma_rate(int M, int N, int a_mn_major, int n
     INFCL_CUDA_TRY(cudaFuncSetAttribute(probe_rate_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65 * 1024));
     INFCL_CUDA_TRY(cudaLaunchKernelEx(&cfg, probe_rate_kernel<1>, M, N, a_mn_major, iters, out_cycles));
   } else {
-    INFCL_CUDA_TRY(cudaFuncSetAttribute(probe_rate_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65 * 1024));
+    INFCL_CUDA_TRY(cudaFuncSetAttribute(probe_rate_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 193 * 1024));
     INFCL_CUDA_TRY(cudaLaunchKernelEx(&cfg, probe_rate_kernel<2>, M, N, a_mn_major, iters, out_cycles));
   }
   return INFCL_OK;
@@ -461,7 +494,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
     for (int i = 0; i < 16; ++i) mbar_init(&ring[i], 1);
-    mbar_init(&done, 1);
+    mbar_init(&done, ((mode & 524288) && !(mode & 32)) ? 2 : 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<2>(&tmem_base, 512);
@@ -546,7 +579,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       mbar_init(&sfull[i], 1);
       mbar_init(&sfree[i], 16);
     }
-    mbar_init(&done, 1);
+    mbar_init(&done, ((mode & 524288) && !(mode & 32)) ? 2 : 1);
     fence_mbar_init();
   }
   if (warp == 9) tmem_alloc<2>(&tmem_base, 512);
@@ -556,7 +589,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   const uint32_t tbase = tmem_base;
   const int KC = KB / 2;
   const long long nst = (long long)tiles * KC;
-  if (warp == 9 && cta == 0) {
+  // mode 524288: TWO issuing warps (9 and 7, different SM sub-partitions) take alternate ring stages (each waits for
+  // and commits its own stages; results invalid -- both accumulate into the same D -- timing only)
+  const bool two = (mode & 524288) != 0 && !(mode & 32);
+  if ((warp == 9 || (two && warp == 7)) && cta == 0) {
+    const int me = warp == 7 ? 1 : 0;
     const bool st = (mode & 2048) != 0;  // S^T shape: M=256 (stage rows) x N=128 (sA rows), same bytes per stage
     const uint32_t idS = st ? idesc_bf16(256, 128, 0, 0) : idesc_bf16(wide ? 256 : 128, 256, 0, 0);
     int stage = 0;
@@ -569,21 +606,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         mbar_wait_cluster(&sfree[buf], ((sfph >> buf) & 1u) ^ 1u);
         sfph ^= 1u << buf;
       }
-      tc_fence_after();
-      const uint32_t dS = tbase + buf * (wide ? 256 : 128);
+      if (!(mode & 8192)) tc_fence_after();
+      // bisection bits: 8192 no tcgen05 fences, 16384 fixed D, 32768 always accumulate, 65536 no per-stage commits
+      const uint32_t dS = (mode & 16384) ? tbase : tbase + buf * (wide ? 256 : 128);
       for (int kc = 0; kc < KC; ++kc) {
+        if (two && (int)(n & 1) != me) {  // the other issuer's stage
+          ++n;
+          if (++stage == ns) {
+            stage = 0;
+            ph ^= 1;
+          }
+          continue;
+        }
         if (mode & 16) mbar_wait(&full[stage], ph);
         else if (n >= ns && !(mode & 128)) mbar_wait(&empty[(mode & 1024) ? (stage & ~1) : stage], ph ^ 1);
-        tc_fence_after();
+        if (!(mode & 8192)) tc_fence_after();
+        const uint32_t acc = (mode & 32768) ? 1u : (kc != 0 ? 1u : 0u);
         const uint64_t ad0 = smem_desc_sw128(smem_u32(sA + 2 * kc * (wide ? 16384 : 8192)), 16, 1024);
         const uint64_t bd0 = smem_desc_sw128(smem_u32(sB + stage * 32768), 16, 1024);
-        if (wide) umma_stage_pair<true, (16384 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
-        else if (st) umma_stage_pair<true, (16384 >> 4), (8192 >> 4)>(dS, (uint32_t)bd0, (uint32_t)ad0, idS, kc != 0);
+        if (wide) umma_stage_pair<true, (16384 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, acc);
+        else if (st) umma_stage_pair<true, (16384 >> 4), (8192 >> 4)>(dS, (uint32_t)bd0, (uint32_t)ad0, idS, acc);
         else if (mode & 4096)  // TS form: A (garbage) in TMEM columns 384.., B = the stage as an MN-major operand
           umma_stage_dI_ts_pair(dS, tbase + 384, (uint32_t)smem_desc_sw128(smem_u32(sB + stage * 32768), 16384, 1024),
-                                idesc_bf16(128, 256, 0, 1), kc != 0);
-        else umma_stage_pair<true, (8192 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, kc != 0);
-        if (mode & 1024) {  // ONE commit per two stages: empty[even] covers the pair
+                                idesc_bf16(128, 256, 0, 1), acc);
+        else if (mode & 131072) {  // issue style L: 8 single-MMA asm statements, 64-bit descriptors from C++
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            umma_bf16_warp<2>(dS, ad0 + (uint64_t)((k >> 2) * (8192 >> 4) + 2 * (k & 3)),
+                              bd0 + (uint64_t)((k >> 2) * (16384 >> 4) + 2 * (k & 3)), idS, k == 0 ? acc : 1u);
+        } else if (mode & 262144) {  // issue style E: one elected lane issues all 8 (plain asm), then the warp syncs
+          uint32_t el;
+          asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(el));
+          if (el) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              umma_bf16<2>(dS, ad0 + (uint64_t)((k >> 2) * (8192 >> 4) + 2 * (k & 3)),
+                           bd0 + (uint64_t)((k >> 2) * (16384 >> 4) + 2 * (k & 3)), idS, k == 0 ? acc : 1u);
+          }
+          __syncwarp();
+        } else umma_stage_pair<true, (8192 >> 4), (16384 >> 4)>(dS, (uint32_t)ad0, (uint32_t)bd0, idS, acc);
+        if (mode & 65536) {
+          // no per-stage commits (only with mode 128: nothing waits for them)
+        } else if (mode & 1024) {  // ONE commit per two stages: empty[even] covers the pair
           if (stage & 1) umma_commit_pair_mc_warp(&empty[stage - 1], 0x3);
         } else if (!(mode & 256)) {
           umma_commit_pair_mc_warp(&empty[stage], 0x3);
@@ -603,7 +667,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     umma_commit_pair_mc_warp(&done, 0x3);
     mbar_wait(&done, 0);
     const long long t2 = clock64();
-    if (lane == 0 && blockIdx.x == 0) {
+    if (lane == 0 && blockIdx.x == 0 && warp == 9) {
       out[0] = t1 - t0;
       out[1] = t2 - t0;
     }
