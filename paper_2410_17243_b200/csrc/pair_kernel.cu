@@ -857,7 +857,10 @@ GcPlan gc_plan(int nrows, int ncols, int dk) {
     const long long items = (long long)waves * g.n_ct * nparts;
     const double cons = (double)((items + pc - 1) / pc) * ((double)g.n_rb / waves) * ((double)NDC / nparts);
     const double cost = std::max(prod, cons);
-    if (cost < best - 1e-9) {
+    // ties go to MORE consumers: a producer that does not remove a wave only shortens the last one, while each extra
+    // consumer lightens every wave's dT work (cfg2: 22 consumers 10.67 ms vs 21 11.19 ms, medians of 4 x 7 steps,
+    // scripts/experiments/gc_split_ab.sh)
+    if (cost <= best + 1e-9) {
       best = cost;
       best_pc = pc;
     }
