@@ -832,10 +832,11 @@ GcPlan gc_plan(int nrows, int ncols, int dk) {
     return e && atoi(e) == 0;
   }();
   const PassGeom g = pass_geom(nrows, ncols);
-  // below ~32K rows per launch the producer / consumer pipeline's fill and drain cost more than the saved S
-  // recompute (virtual ring at cfg2: n = 4 (b_s = 16384) 20.1 ms fused vs 18.5 two-pass; n = 2 (b_s = 32768)
-  // 14.9 vs 15.3); INFCL_GC_MIN_ROWS overrides (tests force the fused kernel at small shapes)
-  long long min_rows = 32768;
+  // below ~16K rows per launch the producer / consumer pipeline's fill and drain cost more than the saved S
+  // recompute (virtual ring at cfg2, final round-2 build with the consumer tie-break: n = 4 (b_s = 16384) 12.7 ms
+  // fused vs 14.7 two-pass, n = 8 (b_s = 8192) 18.3 vs 18.1; earlier builds crossed over at 32K rows);
+  // INFCL_GC_MIN_ROWS overrides (tests force the fused kernel at small shapes)
+  long long min_rows = 16384;
   if (const char* e = getenv("INFCL_GC_MIN_ROWS")) min_rows = atoll(e);
   if (off || dk > kMaxD || g.npairs < 2 || nrows < min_rows) return q;
   const int nparts = dk > 512 ? 2 : 1;  // consumer units per column tile (weights 2 : 1 when split)

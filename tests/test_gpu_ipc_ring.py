@@ -66,7 +66,7 @@ def _worker(rank, world, port, b, d, s, dtype_name, outdir, fused=False):
                                                         (4 * 1500, 768, 4, "bf16", True)])
 def test_ipc_ring_multiprocess(tmp_path, b, d, world, dtype_name, fused):
     """fused: the single-pass backward ring whose dT partials travel (forced at these small shards; the default
-    uses it from 32K rows per rank); otherwise the two-pass backward ring."""
+    uses it from 16K rows per rank); otherwise the two-pass backward ring."""
     import oracle
     from synth import make_features
     s = 14.2857

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(autouse=True)
 def _fused_at_small_shapes(monkeypatch):
-    """The default backward switches to the fused single-pass kernel from 32K rows per launch (DESIGN.md section 5);
+    """The default backward switches to the fused single-pass kernel from 16K rows per launch (DESIGN.md section 5);
     this module's shapes are smaller, so it forces the fused kernel for them (the two-pass path keeps its own tests:
     test_two_pass_backward_world1, the e2e entry, the IPC ring tests without `fused`)."""
     monkeypatch.setenv("INFCL_GC_MIN_ROWS", "0")
