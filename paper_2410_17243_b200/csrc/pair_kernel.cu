@@ -840,9 +840,10 @@ GcPlan gc_plan(int nrows, int ncols, int dk) {
   if (const char* e = getenv("INFCL_GC_MIN_ROWS")) min_rows = atoll(e);
   if (off || dk > kMaxD || g.npairs < 2 || nrows < min_rows) return q;
   const int nparts = dk > 512 ? 2 : 1;  // consumer units per column tile (weights 2 : 1 when split)
-  // producer tile time in consumer-chunk units x NDC: measured optima 22 consumers at d = 512 (2.5), 23-25 at
-  // d = 768 (2.0)
-  double ratio = dk > 512 ? 2.0 : 2.5;
+  // producer tile time in consumer-chunk units x NDC (2.2 at d = 512 and 768): consumer-count sweeps of the final
+  // round-2 build (profiles/gc_split_r02.log) put the optimum at 22 (b = 65536) and 23 (b = 262144) consumers at
+  // d = 512, 25-27 (b = 65536) and 23 (b = 262144) at d = 768
+  double ratio = 2.2;
   if (const char* e = getenv("INFCL_GC_RATIO")) ratio = std::max(0.1, atof(e));
   int best_pc = 1;
   double best = 1e300;
