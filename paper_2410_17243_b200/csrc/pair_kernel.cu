@@ -873,7 +873,9 @@ GcPlan gc_plan(int nrows, int ncols, int dk) {
   q.pc = best_pc;
   q.pp = g.npairs - best_pc;
   q.n_steps = (long long)((g.n_rb + q.pp - 1) / q.pp) * g.n_ct;
-  long long ring = q.pc + 12;
+  // P_c + 4 steps: a smaller ring stays in L2 longer (G ring depth sweeps, profiles/gc_split_r02.log: b = 262144
+  // P_c + 1..4 178-179 ms vs P_c + 11 185 ms; cfg2 and d = 768 within the run-to-run spread or slightly better)
+  long long ring = q.pc + 4;
   // >= 2: a store warp signals step g - 1 only after storing step g, which waits for step g - ring to be read
   if (const char* e = getenv("INFCL_GC_RING")) ring = std::max(2, atoi(e));
   q.ring = (int)std::min<long long>(ring, q.n_steps);
