@@ -1631,9 +1631,104 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     INFCL_CUDA_TRY(cudaEventRecord(evs[8], st));
     INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[8], 0));
     INFCL_CUDA_TRY(cudaMemcpyAsync(loss_host, lg, sizeof(float), cudaMemcpyDeviceToHost, cout));
-    // dI pass (whole), then copy dI out while the dT pass runs chunk by chunk.  (A hybrid -- a fused launch over I
-    // rows [0, 10/16 b), then these two-pass pieces over the remaining rows -- measured the same 17.0 ms: the 268 MB
-    // copy-out at PCIe rates is the bound once the first gradient rows are ready.)
+    // Hybrid backward (INFCL_E2E_HYBRID, default on): one fused single-pass launch over I rows [0, f) x all T
+    // columns (dI rows [0, f) final, their dT contributions accumulated), then the two-pass pieces restricted to
+    // the remaining I rows [f, b): the dI pass over them, and the dT pass in T-row chunks streaming only those I
+    // rows -- gradient rows still finish progressively for the copy-out, and the first 10/16 of the work runs at the
+    // fused kernel's rate.  Otherwise: the dI pass (whole), then dI copied out while the dT pass runs chunk by chunk.
+    static const bool hybrid = [] {
+      const char* e = getenv("INFCL_E2E_HYBRID");
+      return !(e && atoi(e) == 0);
+    }();
+    const int64_t fsplit = at16(10);
+    if (hybrid && fsplit < b && gc_plan((int)fsplit, R.L.bs, R.L.dk).ok) {
+      TRY(bwd_begin(R, r, c, dg, lg + 1, dI, st));
+      diag_init(R, 1, dT, dg, r, c, lg + 1, st);
+      const float coef = (float)((double)R.s / (2.0 * (double)R.b));
+      PassArgs fa{};
+      fa.A = R.A;
+      fa.B = R.B;
+      fa.nrows = (int)fsplit;
+      fa.ncols = R.L.bs;
+      fa.dk = fa.ld = R.L.dk;
+      fa.scale = R.s;
+      fa.diag_on = 1;
+      fa.lse_row2 = R.own2(0);
+      fa.lse_col2 = R.own2(1);
+      fa.dA = dI;
+      fa.ld_dA = R.L.d;
+      fa.d_out = R.L.dk;
+      fa.grad = lg + 1;
+      fa.coef_base = coef;
+      fa.dB = dT;
+      fa.ld_dB = R.L.d;
+      fa.gc_ws = R.ws + R.L.off_slots;
+      fa.gc_ws_bytes = R.L.gc_bytes();
+      const infcl_status fs = launch_pair_backward_fused(fa, st);
+      if (fs == INFCL_OK) {
+        INFCL_CUDA_TRY(cudaEventRecord(evs[9], st));
+        INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[9], 0));
+        INFCL_CUDA_TRY(cudaMemcpyAsync(dI_host, dI, (size_t)fsplit * d * 4, cudaMemcpyDeviceToHost, cout));
+        // dI pass over I rows [f, b): stationary rows f.., all T columns; the positive pair of local row i is column
+        // f + i
+        PassArgs da{};
+        da.A = R.A + (size_t)fsplit * R.L.dk;
+        da.B = R.B;
+        da.nrows = (int)(b - fsplit);
+        da.ncols = R.L.bs;
+        da.dk = da.ld = R.L.dk;
+        da.scale = R.s;
+        da.diag_on = 1;
+        da.row_off = (int)fsplit;
+        da.lse_row2 = R.own2(0) + fsplit;
+        da.lse_col2 = R.own2(1);
+        da.dA = dI + (size_t)fsplit * d;
+        da.ld_dA = R.L.d;
+        da.d_out = R.L.dk;
+        da.grad = lg + 1;
+        da.coef_base = coef;
+        da.tail_scratch = R.tails();
+        TRY(launch_pair_backward(da, st));
+        INFCL_CUDA_TRY(cudaEventRecord(evs[10], st));
+        INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[10], 0));
+        INFCL_CUDA_TRY(cudaMemcpyAsync(dI_host + (size_t)fsplit * d, dI + (size_t)fsplit * d,
+                                       (size_t)(b - fsplit) * d * 4, cudaMemcpyDeviceToHost, cout));
+        // dT pass in T-row chunks over the remaining I rows [f, b) (the fused launch added rows [0, f)); the positive
+        // pair of T row j is streamed column j - f
+        for (int k = 0; k < nch; ++k) {
+          const int r0 = (int)dT_cut[k], r1 = (int)dT_cut[k + 1];
+          if (r1 <= r0) continue;
+          PassArgs ta{};
+          ta.A = R.B + (size_t)r0 * R.L.dk;
+          ta.B = R.A + (size_t)fsplit * R.L.dk;
+          ta.nrows = r1 - r0;
+          ta.ncols = (int)(b - fsplit);
+          ta.dk = ta.ld = R.L.dk;
+          ta.scale = R.s;
+          ta.diag_on = 1;
+          ta.row_off = r0 - (int)fsplit;
+          ta.lse_row2 = R.own2(1) + r0;
+          ta.lse_col2 = R.own2(0) + fsplit;
+          ta.dA = dT + (size_t)r0 * d;
+          ta.ld_dA = R.L.d;
+          ta.d_out = R.L.dk;
+          ta.grad = lg + 1;
+          ta.coef_base = coef;
+          ta.tail_scratch = R.tails();
+          TRY(launch_pair_backward(ta, st));
+          INFCL_CUDA_TRY(cudaEventRecord(evs[12 + k], st));
+          INFCL_CUDA_TRY(cudaStreamWaitEvent(cout, evs[12 + k], 0));
+          INFCL_CUDA_TRY(cudaMemcpyAsync(dT_host + (size_t)r0 * d, dT + (size_t)r0 * d, (size_t)(r1 - r0) * d * 4,
+                                         cudaMemcpyDeviceToHost, cout));
+        }
+        INFCL_CUDA_TRY(cudaEventRecord(evs[20], cout));
+        INFCL_CUDA_TRY(cudaStreamWaitEvent(st, evs[20], 0));  // the call's stream orders after every copy
+        INFCL_CUDA_TRY(cudaStreamSynchronize(st));
+        return INFCL_OK;
+      }
+      if (fs != INFCL_ERR_UNSUPPORTED) return fs;
+      // not all CTA pairs co-resident: the two passes below (they re-initialise dI and dT)
+    }
     TRY(bwd_begin(R, r, c, dg, lg + 1, dI, st));
     TRY(bwd_step(R, R.A, R.own2(0), R.B, R.own2(1), true, dI, d, lg + 1, st));
     TRY(pass_end(R, 0, dI, dg, r, c, lg + 1, st));
