@@ -1634,13 +1634,19 @@ extern "C" infcl_status infcl_loss_grad_host(const void* I_host, const void* T_h
     // Hybrid backward (INFCL_E2E_HYBRID, default on): one fused single-pass launch over I rows [0, f) x all T
     // columns (dI rows [0, f) final, their dT contributions accumulated), then the two-pass pieces restricted to
     // the remaining I rows [f, b): the dI pass over them, and the dT pass in T-row chunks streaming only those I
-    // rows -- gradient rows still finish progressively for the copy-out, and the first 10/16 of the work runs at the
+    // rows -- gradient rows still finish progressively for the copy-out, and the first half of the work runs at the
     // fused kernel's rate.  Otherwise: the dI pass (whole), then dI copied out while the dT pass runs chunk by chunk.
     static const bool hybrid = [] {
       const char* e = getenv("INFCL_E2E_HYBRID");
       return !(e && atoi(e) == 0);
     }();
-    const int64_t fsplit = at16(10);
+    // the fused part: 8/16 of b (A/B over 5-12 sixteenths, scripts/experiments/e2e_fsplit.sh: 8 best; the tests
+    // sample the rows around this split, tests/test_gpu_large.py e2e_boundaries); INFCL_E2E_FSPLIT overrides
+    static const int fsix = [] {
+      const char* e = getenv("INFCL_E2E_FSPLIT");
+      return e ? std::max(1, std::min(15, atoi(e))) : 8;
+    }();
+    const int64_t fsplit = at16(fsix);
     if (hybrid && fsplit < b && gc_plan((int)fsplit, R.L.bs, R.L.dk).ok) {
       TRY(bwd_begin(R, r, c, dg, lg + 1, dI, st));
       diag_init(R, 1, dT, dg, r, c, lg + 1, st);

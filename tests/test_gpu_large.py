@@ -113,8 +113,9 @@ def test_cfg3_codebook_closed_form():
 
 def e2e_boundaries(b):
     """Row / column boundaries of infcl_loss_grad_host's pipelined schedule (api.cu: forward I chunks at
-    sixteenths {1, 4, 10}, dT-pass chunks at {6, 11, 15}, 128-row aligned; T split at 3/8, 256 aligned)."""
-    at16 = [min(b, (b * e // 16 + 127) // 128 * 128) for e in (1, 4, 6, 10, 11, 15)]
+    sixteenths {1, 4, 10}, the hybrid backward's fused / two-pass split at 8, dT-pass chunks at {6, 11, 15},
+    128-row aligned; T split at 3/8, 256 aligned)."""
+    at16 = [min(b, (b * e // 16 + 127) // 128 * 128) for e in (1, 4, 6, 8, 10, 11, 15)]
     return at16 + [min(b, (b * 3 // 8 + 255) // 256 * 256)]
 
 
